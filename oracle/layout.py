@@ -1,0 +1,110 @@
+"""Length bucketing, tile plan and shard plan (oracle, plain Python).
+
+PAPER.md:367-369 ("Batched projection operator"): slices are grouped by length
+into logarithmic buckets [2^(t-1), 2^t), so a block of length s >= 1 lies in
+bucket t = floor(log2 s) + 1 and the number of buckets (GPU launches in the
+paper) is at most 1 + floor(log2 s_max).
+
+This framework keeps the buckets but, instead of padded dense slabs, lays the
+blocks out bucket-contiguously in HBM and cuts each bucket into *tiles*
+(reading R10):
+
+* blocks of length 0 are skipped (PAPER.md silent; they carry no variables);
+* blocks are ordered by (bucket descending, source id ascending);
+* a bucket t >= BIG_BUCKET (length >= 256) block is a tile of its own, worked
+  by a multi-warp group; smaller buckets are packed greedily, in that order,
+  into tiles of at most ``tile_cap`` entries;
+* every tile starts at an entry offset that is a multiple of 4 (16-byte TMA
+  alignment); blocks inside a tile are contiguous.
+
+Shard plan ("balanced column split"): rank w of W owns the
+contiguous sources [B_w, B_{w+1}) with B_w the first source whose CSR offset
+reaches floor(w * nnz / W).
+"""
+from __future__ import annotations
+
+import math
+
+BIG_BUCKET = 9      # buckets >= 9 (length >= 256) are worked by multi-warp groups
+ALIGN = 4           # entries (16 bytes of int32/float32)
+
+
+def bucket_of(s: int) -> int:
+    """t = floor(log2 s) + 1, i.e. s in [2^(t-1), 2^t)."""
+    if s < 1:
+        raise ValueError("empty block has no bucket")
+    return int(math.floor(math.log2(s))) + 1
+
+
+def bucket_plan(lengths):
+    """Paper's plan: {t: [block ids ascending]} and its launch count."""
+    plan = {}
+    for i, s in enumerate(lengths):
+        if s > 0:
+            plan.setdefault(bucket_of(int(s)), []).append(i)
+    return dict(sorted(plan.items())), len(plan)
+
+
+def group_lanes(t: int) -> int:
+    """Lanes cooperating on one block of bucket t: 1 for t<=3, else 2^(t-3), at most 512."""
+    return 1 if t <= 3 else min(2 ** (t - 3), 512)
+
+
+def tile_plan(lengths, tile_cap: int):
+    """Returns (perm, blk_off, tiles, total) -- see module docstring.
+
+    perm[b]    source id of the b-th block in layout order
+    blk_off[b] entry offset of that block in the permuted arrays
+    tiles      list of (first_block, num_blocks, entry_offset, num_entries, bucket)
+    total      entries of the permuted arrays (including alignment gaps)
+    """
+    buckets, _ = bucket_plan(lengths)
+    perm, blk_off, tiles = [], [], []
+    off = 0
+    for t in sorted(buckets, reverse=True):
+        members = buckets[t]
+        groups = []
+        if t >= BIG_BUCKET:
+            groups = [[i] for i in members]
+        else:
+            cur, cur_n = [], 0
+            for i in members:
+                s = int(lengths[i])
+                if cur and cur_n + s > tile_cap:
+                    groups.append(cur)
+                    cur, cur_n = [], 0
+                cur.append(i)
+                cur_n += s
+            if cur:
+                groups.append(cur)
+        for grp in groups:
+            off = (off + ALIGN - 1) // ALIGN * ALIGN
+            start, b0 = off, len(perm)
+            for i in grp:
+                perm.append(i)
+                blk_off.append(off)
+                off += int(lengths[i])
+            tiles.append((b0, len(grp), start, off - start, t))
+    return perm, blk_off, tiles, off
+
+
+def shard_bounds(row_ptr, world: int):
+    """[B_0=0, B_1, ..., B_W=I] with B_w = min{i : row_ptr[i] >= floor(w*nnz/W)}."""
+    I = len(row_ptr) - 1
+    nnz = int(row_ptr[-1])
+    out = [0]
+    for w in range(1, world):
+        target = (w * nnz) // world
+        lo, hi = 0, I
+        while lo < hi:                       # first i with row_ptr[i] >= target
+            mid = (lo + hi) // 2
+            if int(row_ptr[mid]) >= target:
+                hi = mid
+            else:
+                lo = mid + 1
+        out.append(max(lo, out[-1]))
+    out.append(I)
+    return out
+
+
+__all__ = ["BIG_BUCKET", "ALIGN", "bucket_of", "bucket_plan", "group_lanes", "tile_plan", "shard_bounds"]

@@ -1,0 +1,95 @@
+"""Pins for oracle.layout: the paper's bucket bracket and launch bound
+(PAPER.md:369), the tile-plan invariants of DESIGN.md "HBM layout", and the
+shard-plan balance."""
+import math
+
+import numpy as np
+
+from oracle.layout import ALIGN, BIG_BUCKET, bucket_of, bucket_plan, group_lanes, shard_bounds, tile_plan
+
+
+def test_bucket_bracket():
+    for s in range(1, 5000):
+        t = bucket_of(s)
+        assert 2 ** (t - 1) <= s < 2 ** t
+
+
+def test_paper_example_buckets():
+    """lengths [1,2,3,5,8] -> {1}, {2,3}, {5}, {8}; 4 launches = 1 + floor(log2 8)."""
+    plan, launches = bucket_plan([1, 2, 3, 5, 8])
+    assert plan == {1: [0], 2: [1, 2], 3: [3], 4: [4]}
+    assert launches == 4 == 1 + math.floor(math.log2(8))
+    assert bucket_plan([1, 1, 1]) == ({1: [0, 1, 2]}, 1)
+    assert bucket_plan([]) == ({}, 0)
+    assert bucket_plan([0, 0, 3]) == ({2: [2]}, 1)       # empty blocks skipped
+
+
+def test_launch_bound_and_padding_bound():
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        lens = rng.integers(0, 3000, rng.integers(1, 300))
+        plan, launches = bucket_plan(lens)
+        if lens.max() > 0:
+            assert launches <= 1 + math.floor(math.log2(lens.max()))
+        for t, ids in plan.items():  # padded slab waste < 2x true entries
+            assert len(ids) * (2 ** t - 1) < 2 * lens[ids].sum()
+
+
+def test_group_lanes_hold_block_in_8_per_lane():
+    for t in range(1, 13):
+        assert math.ceil((2 ** t - 1) / group_lanes(t)) <= 8
+
+
+def test_tile_plan_invariants():
+    rng = np.random.default_rng(1)
+    for trial in range(60):
+        n = int(rng.integers(1, 2000))
+        if trial % 3 == 0:
+            lens = np.minimum((rng.pareto(1.0, n) + 1).astype(int), 5000)
+        else:
+            lens = rng.poisson(rng.choice([3, 40, 120]), n)
+        lens[rng.random(n) < 0.05] = 0
+        cap = int(rng.choice([256, 424, 512, 1024]))
+        perm, off, tiles, total = tile_plan(lens, cap)
+        nz = np.flatnonzero(lens > 0)
+        assert sorted(perm) == list(nz)                                # every nonempty block once
+        keys = [(-bucket_of(int(lens[i])), i) for i in perm]
+        assert keys == sorted(keys)                                    # (bucket desc, id asc)
+        covered = 0
+        for (b0, nb, toff, tn, t) in tiles:
+            assert b0 == covered and nb >= 1
+            covered += nb
+            assert toff % ALIGN == 0
+            members = perm[b0:b0 + nb]
+            assert all(bucket_of(int(lens[i])) == t for i in members)
+            assert off[b0] == toff
+            for q in range(nb - 1):
+                assert off[b0 + q + 1] == off[b0 + q] + lens[members[q]]
+            assert tn == sum(int(lens[i]) for i in members)
+            if t >= BIG_BUCKET:
+                assert nb == 1
+            else:
+                assert tn <= cap
+        assert covered == len(perm)
+        # greedy maximality: the next block of the same bucket did not fit
+        for (a, b) in zip(tiles, tiles[1:]):
+            if a[4] == b[4] and a[4] < BIG_BUCKET:
+                assert a[3] + lens[perm[b[0]]] > cap
+        assert total >= int(lens.sum())
+
+
+def test_shard_bounds():
+    rng = np.random.default_rng(2)
+    for _ in range(100):
+        lens = rng.integers(0, 200, rng.integers(1, 500))
+        if rng.random() < 0.3:
+            lens[rng.integers(0, lens.size)] = 10000
+        rp = np.concatenate([[0], np.cumsum(lens)])
+        for W in (1, 2, 3, 4, 8):
+            B = shard_bounds(rp, W)
+            assert B[0] == 0 and B[-1] == lens.size and all(x <= y for x, y in zip(B, B[1:]))
+            nnz = rp[-1]
+            for w in range(W):
+                shard = rp[B[w + 1]] - rp[B[w]]
+                assert shard <= math.ceil(nnz / W) + lens.max()
+    assert shard_bounds(np.arange(0, 101, 1), 4) == [0, 25, 50, 75, 100]
