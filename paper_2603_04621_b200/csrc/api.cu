@@ -1,0 +1,783 @@
+// C ABI (include/dualip.h): problem lifetime, layout build, gradient / AGD / solve
+// entry points, CUDA-graph capture of the iteration, NCCL (dlopen) all-reduce.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+// Minimal NCCL surface (types from nccl.h; functions resolved with dlsym).
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { kNcclFloat64 = 8, kNcclSum = 0 };
+
+namespace dl {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+struct Nccl {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+static Nccl g_nccl;
+
+static bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    set_error(std::string("NCCL not loadable (dlopen libnccl.so.2): ") + dlerror());
+    return false;
+  }
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+  if (!g_nccl.ok) set_error("NCCL symbols missing");
+  return g_nccl.ok;
+}
+
+}  // namespace dl
+
+using namespace dl;
+
+struct dl_problem {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t I = 0, nnz = 0;
+  int32_t J = 0, M = 1, kind = 0;
+  float r = 1.f, u = INFINITY;
+  // layout
+  Plan plan;
+  int32_t tile_cap = 256, lam_smem = 0, num_sms = 148, ctas = 148;
+  size_t smem = 0;
+  int64_t nnz_layout = 0, a_stride = 0;
+  int32_t* d_dest = nullptr;
+  float *d_c = nullptr, *d_a = nullptr, *d_b = nullptr, *d_vsq = nullptr, *d_vinv = nullptr;
+  Tile* d_tiles = nullptr;
+  uint16_t* d_blk_rel = nullptr;
+  int64_t* d_orig_off = nullptr;
+  double* d_gscratch = nullptr;
+  int64_t gscratch_per_cta = 0;
+  float cmax = 0.f, amax[4] = {0.f, 0.f, 0.f, 0.f};
+  float* d_slack = nullptr;  // [2]: 0 standalone path, 1 solver path
+  // work
+  double* d_acc = nullptr;   // [MJ + 4]
+  int32_t* d_ctr = nullptr;  // [8]
+  // standalone grad path
+  float* d_lam_in = nullptr;
+  double *d_grad_out = nullptr, *d_obj_out = nullptr;
+  float* h_lam_pin = nullptr;
+  double* h_out_pin = nullptr;
+  // Jacobi
+  double* d_D = nullptr;
+  double* d_Dones = nullptr;
+  bool jacobi_set = false;
+  // AGD
+  bool agd_ready = false;
+  dl_agd_params prm{};
+  double *d_lam1 = nullptr, *d_lam2 = nullptr, *d_lam2_prev = nullptr, *d_G_prev = nullptr;
+  float* d_mu = nullptr;
+  AgdDev* d_st = nullptr;
+  dl_iter_record* d_hist = nullptr;
+  int64_t hist_cap = 0;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  int graph_iters = 0;
+  // NCCL
+  ncclComm_t comm = nullptr;
+  int32_t rank = 0, world = 1;
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+#define CUDA_TRY(expr)                                                                       \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess) {                                                                 \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));                         \
+      return _e == cudaErrorMemoryAllocation ? DL_ERR_OOM : DL_ERR_CUDA;                      \
+    }                                                                                        \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    cudaGetDevice(&prev);
+    if (prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+dl_status dev_alloc(dl_problem* p, T** ptr, size_t count) {
+  size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    cudaGetLastError();
+    return DL_ERR_OOM;
+  }
+  p->allocs.push_back(q);
+  p->device_bytes += (int64_t)bytes;
+  *ptr = static_cast<T*>(q);
+  return DL_OK;
+}
+
+#define DL_TRY(expr)                  \
+  do {                                \
+    dl_status _s = (expr);            \
+    if (_s != DL_OK) return _s;       \
+  } while (0)
+
+void free_all(dl_problem* p) {
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  p->graph = nullptr;
+  for (void* q : p->allocs) cudaFree(q);
+  p->allocs.clear();
+  if (p->h_lam_pin) cudaFreeHost(p->h_lam_pin);
+  if (p->h_out_pin) cudaFreeHost(p->h_out_pin);
+  if (p->comm && g_nccl.ok) g_nccl.CommDestroy(p->comm);
+  if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
+}
+
+GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, double gamma_val, float* x_out,
+                   const float* slack) {
+  GradArgs a{};
+  a.slack = slack;
+  a.dest = p->d_dest;
+  a.c = p->d_c;
+  a.a = p->d_a;
+  a.a_stride = p->a_stride;
+  a.tiles = p->d_tiles;
+  for (int i = 0; i < kNumBigPhases + 2; ++i) a.ph_begin[i] = p->plan.ph_begin[i];
+  a.blk_rel = p->d_blk_rel;
+  a.vsq = p->d_vsq;
+  a.vinv = p->d_vinv;
+  a.orig_off = p->d_orig_off;
+  a.lam = lam;
+  a.J = p->J;
+  a.m = p->M;
+  a.gamma_ptr = gamma_ptr;
+  a.gamma_val = gamma_val;
+  a.r = p->r;
+  a.u = p->u;
+  a.kind = p->kind;
+  a.tile_cap = p->tile_cap;
+  a.lam_smem = p->lam_smem;
+  a.acc = p->d_acc;
+  a.ctr = p->d_ctr;
+  a.x_out = x_out;
+  a.gscratch = p->d_gscratch;
+  a.gscratch_per_cta = p->gscratch_per_cta;
+  return a;
+}
+
+dl_status run_grad(dl_problem* p, const float* lam, const double* gamma_ptr, double gamma_val, float* x_out,
+                   bool zero_first) {
+  const int64_t n = (int64_t)p->M * p->J;
+  if (zero_first) {
+    CUDA_TRY(cudaMemsetAsync(p->d_acc, 0, (n + 4) * sizeof(double), p->stream));
+    CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, 8 * sizeof(int32_t), p->stream));
+  }
+  if (p->plan.tiles.empty()) return DL_OK;
+  const float* slack = p->d_slack + 1;  // solver path: written by the step kernel
+  if (zero_first) {                      // standalone path: bound for this lambda
+    CUDA_TRY(launch_slack(lam, p->M, p->J, p->cmax, p->amax, p->d_slack, p->stream));
+    slack = p->d_slack;
+  }
+  CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out, slack), p->ctas, p->smem, p->stream));
+  return DL_OK;
+}
+
+StepArgs step_args(dl_problem* p) {
+  StepArgs s{};
+  s.n = p->M * p->J;
+  s.D = p->prm.use_jacobi ? p->d_D : p->d_Dones;
+  s.b = p->d_b;
+  s.acc = p->d_acc;
+  s.ctr = p->d_ctr;
+  s.lam1 = p->d_lam1;
+  s.lam2 = p->d_lam2;
+  s.lam2_prev = p->d_lam2_prev;
+  s.G_prev = p->d_G_prev;
+  s.mu = p->d_mu;
+  s.st = p->d_st;
+  s.hist = p->d_hist;
+  s.m = p->M;
+  s.cmax = p->cmax;
+  for (int f = 0; f < 4; ++f) s.amax[f] = p->amax[f];
+  s.slack = p->d_slack + 1;
+  return s;
+}
+
+dl_status enqueue_iteration(dl_problem* p) {
+  DL_TRY(run_grad(p, p->d_mu, &p->d_st->gamma, 0.0, nullptr, false));
+  if (p->comm) {
+    ncclResult_t r = g_nccl.AllReduce(p->d_acc, p->d_acc, (size_t)p->M * p->J + 4, kNcclFloat64, kNcclSum,
+                                      p->comm, p->stream);
+    if (r != 0) {
+      set_error(std::string("ncclAllReduce: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+      return DL_ERR_NCCL;
+    }
+  }
+  CUDA_TRY(launch_agd_step(step_args(p), p->stream));
+  return DL_OK;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int dl_abi_version(void) { return DL_ABI_VERSION; }
+const char* dl_last_error(void) { return g_err.c_str(); }
+
+dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
+  if (!d || !out) {
+    set_error("dl_problem_create: NULL argument");
+    return DL_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (d->num_sources < 0 || d->num_dests < 1 || d->num_families < 1 || d->num_families > 4 || d->nnz < 0 ||
+      (d->num_sources > 0 && !d->row_ptr) || (d->nnz > 0 && (!d->dest || !d->a || !d->c)) || !d->b ||
+      d->nnz >= (1LL << 40) || d->num_sources >= (1LL << 31)) {
+    set_error("dl_problem_create: invalid sizes or NULL arrays");
+    return DL_ERR_INVALID;
+  }
+  if (d->proj_kind < DL_PROJ_SIMPLEX || d->proj_kind > DL_PROJ_BOX) {
+    set_error("dl_problem_create: unknown proj_kind");
+    return DL_ERR_INVALID;
+  }
+  if ((d->proj_kind != DL_PROJ_BOX && !(d->proj_r > 0)) || (d->proj_kind != DL_PROJ_SIMPLEX && !(d->proj_u > 0))) {
+    set_error("dl_problem_create: caps must be positive (r for simplex/box-cut, u for box-cut/box)");
+    return DL_ERR_INVALID;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || d->device < 0 || d->device >= ndev) {
+    cudaGetLastError();
+    set_error("dl_problem_create: no CUDA device (there is no CPU fallback)");
+    return DL_ERR_CUDA;
+  }
+  DeviceGuard guard(d->device);
+  dl_problem* p = new dl_problem();
+  p->device = d->device;
+  p->I = d->num_sources;
+  p->nnz = d->nnz;
+  p->J = d->num_dests;
+  p->M = d->num_families;
+  p->kind = d->proj_kind;
+  p->r = d->proj_kind == DL_PROJ_BOX ? INFINITY : (float)d->proj_r;
+  p->u = d->proj_kind == DL_PROJ_SIMPLEX ? INFINITY : (float)d->proj_u;
+  auto fail = [&](dl_status s) {
+    free_all(p);
+    delete p;
+    return s;
+  };
+  if (d->stream) {
+    p->stream = (cudaStream_t)d->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      set_error("cudaStreamCreate failed");
+      return fail(DL_ERR_CUDA);
+    }
+    p->own_stream = true;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, p->device) != cudaSuccess) return fail(DL_ERR_CUDA);
+  p->num_sms = prop.multiProcessorCount;
+  p->ctas = p->num_sms;
+  int lam_smem = 0;
+  p->tile_cap = tile_cap_rule(p->M, p->J, &lam_smem);
+  p->lam_smem = lam_smem;
+  p->smem = fused_smem_bytes(p->M, p->J, p->tile_cap, lam_smem);
+  if ((size_t)prop.sharedMemPerBlockOptin < p->smem) {
+    set_error("dl_problem_create: device shared memory per block below the layout's need");
+    return fail(DL_ERR_UNSUPPORTED);
+  }
+  // plan on the host from row_ptr
+  std::vector<int64_t> rp((size_t)p->I + 1, 0);
+  if (p->I > 0) {
+    cudaError_t e = cudaMemcpyAsync(rp.data(), d->row_ptr, rp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                    p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) {
+      set_error(std::string("reading row_ptr: ") + cudaGetErrorString(e));
+      return fail(DL_ERR_CUDA);
+    }
+  }
+  if (rp[0] != 0 || rp[(size_t)p->I] != p->nnz) {
+    set_error("dl_problem_create: row_ptr[0] != 0 or row_ptr[I] != nnz");
+    return fail(DL_ERR_INVALID);
+  }
+  for (int64_t i = 0; i < p->I; ++i)
+    if (rp[i + 1] < rp[i]) {
+      set_error("dl_problem_create: row_ptr decreasing");
+      return fail(DL_ERR_INVALID);
+    }
+  p->plan = make_plan(rp.data(), p->I, p->tile_cap);
+  const Plan& P = p->plan;
+  const int64_t nb = (int64_t)P.perm.size(), nt = (int64_t)P.tiles.size();
+  p->nnz_layout = P.total;
+  p->a_stride = (P.total + 2 * kAlign + 31) / 32 * 32;  // room for the last tile's rounded copy
+  const int64_t MJ = (int64_t)p->M * p->J;
+  // device buffers
+  dl_status s;
+  if ((s = dev_alloc(p, &p->d_dest, p->a_stride)) || (s = dev_alloc(p, &p->d_c, p->a_stride)) ||
+      (s = dev_alloc(p, &p->d_a, (size_t)p->a_stride * p->M)) || (s = dev_alloc(p, &p->d_b, MJ)) ||
+      (s = dev_alloc(p, &p->d_tiles, nt)) || (s = dev_alloc(p, &p->d_blk_rel, nb)) ||
+      (s = dev_alloc(p, &p->d_orig_off, nb)) || (s = dev_alloc(p, &p->d_acc, MJ + 4)) ||
+      (s = dev_alloc(p, &p->d_ctr, 8)) || (s = dev_alloc(p, &p->d_D, MJ)) || (s = dev_alloc(p, &p->d_Dones, MJ)) ||
+      (s = dev_alloc(p, &p->d_lam_in, MJ)) || (s = dev_alloc(p, &p->d_grad_out, MJ)) ||
+      (s = dev_alloc(p, &p->d_obj_out, 4)) || (s = dev_alloc(p, &p->d_slack, 2)))
+    return fail(s);
+  if (d->v && ((s = dev_alloc(p, &p->d_vsq, nb)) || (s = dev_alloc(p, &p->d_vinv, nb)))) return fail(s);
+  // global d-scratch for blocks longer than a 16-warp group's shared scratch
+  const int64_t smem_scr = (int64_t)kWarps * 2 * p->tile_cap * (8 + 4 * p->M) / 8;  // fp64 d
+  if (P.max_len > smem_scr) {
+    p->gscratch_per_cta = P.max_len;
+    if ((s = dev_alloc(p, &p->d_gscratch, (size_t)P.max_len * p->ctas))) return fail(s);
+  }
+  if (cudaMallocHost(&p->h_lam_pin, std::max<int64_t>(MJ, 1) * sizeof(float)) != cudaSuccess ||
+      cudaMallocHost(&p->h_out_pin, (MJ + 4) * sizeof(double)) != cudaSuccess) {
+    set_error("cudaMallocHost failed");
+    return fail(DL_ERR_OOM);
+  }
+  // host -> device plan arrays
+  std::vector<uint16_t> rel((size_t)nb, 0);
+  std::vector<int64_t> orig((size_t)nb, 0);
+  for (const Tile& tl : P.tiles)
+    for (int q = 0; q < tl.nb; ++q) rel[tl.b0 + q] = (uint16_t)(tl.bucket >= kBigBucket ? 0 : P.blk_off[tl.b0 + q] - tl.off);
+  for (int64_t b = 0; b < nb; ++b) orig[b] = rp[P.perm[b]];
+  int64_t *d_perm = nullptr, *d_boff = nullptr;
+  if ((s = dev_alloc(p, &d_perm, nb)) || (s = dev_alloc(p, &d_boff, nb))) return fail(s);
+  CUDA_TRY(cudaMemsetAsync(p->d_dest, 0, p->a_stride * sizeof(int32_t), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->d_c, 0, p->a_stride * sizeof(float), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->d_a, 0, (size_t)p->a_stride * p->M * sizeof(float), p->stream));
+  CUDA_TRY(cudaMemcpyAsync(p->d_tiles, P.tiles.data(), nt * sizeof(Tile), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(p->d_blk_rel, rel.data(), nb * sizeof(uint16_t), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(p->d_orig_off, orig.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_perm, P.perm.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(d_boff, P.blk_off.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(p->d_b, d->b, MJ * sizeof(float), cudaMemcpyDeviceToDevice, p->stream));
+  LayoutArgs la{};
+  la.row_ptr = d->row_ptr;
+  la.dest = d->dest;
+  la.a = d->a;
+  la.c = d->c;
+  la.v = d->v;
+  la.nnz = p->nnz;
+  la.a_stride_out = p->a_stride;
+  la.m = p->M;
+  la.num_blocks = nb;
+  la.perm = d_perm;
+  la.blk_off = d_boff;
+  la.dest_out = p->d_dest;
+  la.c_out = p->d_c;
+  la.a_out = p->d_a;
+  la.vsq_out = p->d_vsq;
+  la.vinv_out = p->d_vinv;
+  CUDA_TRY(launch_build_layout(la, p->stream));
+  CUDA_TRY(launch_jacobi_diag(nullptr, p->d_D, (int32_t)MJ, p->stream));
+  CUDA_TRY(launch_jacobi_diag(nullptr, p->d_Dones, (int32_t)MJ, p->stream));
+  // magnitude bounds for the fp32 candidate filter: max|c|, max|a_f|
+  {
+    float* d_mx = nullptr;
+    if ((s = dev_alloc(p, &d_mx, 5))) return fail(s);
+    CUDA_TRY(launch_absmax(p->d_c, p->nnz_layout, d_mx, p->stream));
+    for (int f = 0; f < p->M; ++f)
+      CUDA_TRY(launch_absmax(p->d_a + (size_t)f * p->a_stride, p->nnz_layout, d_mx + 1 + f, p->stream));
+    float mx[5] = {0, 0, 0, 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(mx, d_mx, 5 * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    p->cmax = mx[0];
+    for (int f = 0; f < p->M; ++f) p->amax[f] = mx[1 + f];
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  // temporary plan arrays are not needed any more
+  for (void* q : {(void*)d_perm, (void*)d_boff}) {
+    cudaFree(q);
+    p->allocs.erase(std::find(p->allocs.begin(), p->allocs.end(), q));
+  }
+  p->device_bytes -= 2 * std::max<int64_t>(nb, 1) * (int64_t)sizeof(int64_t);
+  *out = p;
+  return DL_OK;
+}
+
+dl_status dl_problem_destroy(dl_problem* p) {
+  if (!p) return DL_OK;
+  DeviceGuard guard(p->device);
+  cudaStreamSynchronize(p->stream);
+  free_all(p);
+  delete p;
+  return DL_OK;
+}
+
+dl_status dl_problem_get_info(const dl_problem* p, dl_problem_info* o) {
+  if (!p || !o) {
+    set_error("dl_problem_get_info: NULL argument");
+    return DL_ERR_INVALID;
+  }
+  std::memset(o, 0, sizeof(*o));
+  o->num_sources = p->I;
+  o->nnz = p->nnz;
+  o->nnz_layout = p->nnz_layout;
+  o->num_blocks = (int64_t)p->plan.perm.size();
+  o->num_tiles = (int64_t)p->plan.tiles.size();
+  o->num_big_tiles = p->plan.ph_begin[kNumBigPhases];
+  o->num_dests = p->J;
+  o->num_families = p->M;
+  o->tile_cap = p->tile_cap;
+  o->lambda_in_smem = p->lam_smem;
+  o->max_block_len = p->plan.max_len;
+  o->num_buckets = p->plan.num_buckets;
+  o->num_sms = p->num_sms;
+  o->ctas = p->ctas;
+  o->device_bytes = p->device_bytes;
+  return DL_OK;
+}
+
+dl_status dl_problem_layout(const dl_problem* p, int64_t* perm, int64_t* blk_off, int64_t* tiles) {
+  if (!p) {
+    set_error("dl_problem_layout: NULL problem");
+    return DL_ERR_INVALID;
+  }
+  const Plan& P = p->plan;
+  if (perm) std::memcpy(perm, P.perm.data(), P.perm.size() * sizeof(int64_t));
+  if (blk_off) std::memcpy(blk_off, P.blk_off.data(), P.blk_off.size() * sizeof(int64_t));
+  if (tiles) {
+    // read the descriptors back from the device: the layout actually used
+    std::vector<Tile> t(P.tiles.size());
+    DeviceGuard guard(p->device);
+    CUDA_TRY(cudaMemcpy(t.data(), p->d_tiles, t.size() * sizeof(Tile), cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < t.size(); ++q) {
+      tiles[5 * q + 0] = t[q].b0;
+      tiles[5 * q + 1] = t[q].nb;
+      tiles[5 * q + 2] = t[q].off;
+      tiles[5 * q + 3] = t[q].nnz;
+      tiles[5 * q + 4] = t[q].bucket;
+    }
+  }
+  return DL_OK;
+}
+
+dl_status dl_problem_layout_data(const dl_problem* p, int32_t* dest, float* c, float* a) {
+  if (!p) {
+    set_error("dl_problem_layout_data: NULL problem");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  const size_t n = (size_t)p->nnz_layout;
+  if (dest) CUDA_TRY(cudaMemcpy(dest, p->d_dest, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (c) CUDA_TRY(cudaMemcpy(c, p->d_c, n * sizeof(float), cudaMemcpyDeviceToHost));
+  if (a)
+    for (int f = 0; f < p->M; ++f)
+      CUDA_TRY(cudaMemcpy(a + f * n, p->d_a + f * p->a_stride, n * sizeof(float), cudaMemcpyDeviceToHost));
+  return DL_OK;
+}
+
+dl_status dl_row_sqnorms(dl_problem* p, double* out) {
+  if (!p || !out) {
+    set_error("dl_row_sqnorms: NULL argument");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaMemsetAsync(out, 0, (size_t)p->M * p->J * sizeof(double), p->stream));
+  CUDA_TRY(launch_row_sqnorms(p->d_dest, p->d_a, p->a_stride, p->nnz_layout, p->M, p->J, out, p->stream));
+  return DL_OK;
+}
+
+dl_status dl_set_jacobi(dl_problem* p, const double* rowsq) {
+  if (!p) {
+    set_error("dl_set_jacobi: NULL problem");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(launch_jacobi_diag(rowsq, p->d_D, p->M * p->J, p->stream));
+  p->jacobi_set = rowsq != nullptr;
+  return DL_OK;
+}
+
+dl_status dl_dual_grad(dl_problem* p, const float* lam, double gamma, double* grad, double* obj, uint32_t flags) {
+  if (!p || !lam || !grad || !obj || !(gamma > 0)) {
+    set_error("dl_dual_grad: NULL argument or gamma <= 0");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  DL_TRY(run_grad(p, lam, nullptr, gamma, nullptr, true));
+  FinalizeArgs f{p->M * p->J, p->d_acc, p->d_b, lam, grad, obj, (int32_t)(flags & DL_GRAD_PARTIAL)};
+  CUDA_TRY(launch_finalize(f, p->stream));
+  return DL_OK;
+}
+
+dl_status dl_dual_grad_host(dl_problem* p, const float* lam, double gamma, double* grad, double* obj,
+                            uint32_t flags) {
+  if (!p || !lam || !grad || !obj || !(gamma > 0)) {
+    set_error("dl_dual_grad_host: NULL argument or gamma <= 0");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  const size_t n = (size_t)p->M * p->J;
+  CUDA_TRY(cudaMemcpyAsync(p->d_lam_in, lam, n * sizeof(float), cudaMemcpyHostToDevice, p->stream));
+  DL_TRY(dl_dual_grad(p, p->d_lam_in, gamma, p->d_grad_out, p->d_obj_out, flags));
+  CUDA_TRY(cudaMemcpyAsync(grad, p->d_grad_out, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(obj, p->d_obj_out, 4 * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return DL_OK;
+}
+
+dl_status dl_primal(dl_problem* p, const float* lam, double gamma, float* x) {
+  if (!p || !lam || !x || !(gamma > 0)) {
+    set_error("dl_primal: NULL argument or gamma <= 0");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaMemsetAsync(x, 0, (size_t)p->nnz * sizeof(float), p->stream));
+  DL_TRY(run_grad(p, lam, nullptr, gamma, x, true));
+  return DL_OK;
+}
+
+dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm) {
+  if (!p || !prm || !(prm->gamma0 > 0) || !(prm->max_step > 0) || !(prm->init_step > 0) ||
+      (prm->gamma_min > 0 && prm->gamma_min < prm->gamma0 && prm->halve_every < 1)) {
+    set_error("dl_agd_init: invalid parameters");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  const int64_t n = (int64_t)p->M * p->J;
+  if (!p->d_lam1) {
+    dl_status s;
+    if ((s = dev_alloc(p, &p->d_lam1, n)) || (s = dev_alloc(p, &p->d_lam2, n)) ||
+        (s = dev_alloc(p, &p->d_lam2_prev, n)) || (s = dev_alloc(p, &p->d_G_prev, n)) ||
+        (s = dev_alloc(p, &p->d_mu, n)) || (s = dev_alloc(p, &p->d_st, 1)))
+      return s;
+  }
+  const int64_t cap = prm->history_cap > 0 ? prm->history_cap : 65536;
+  if (cap != p->hist_cap) {
+    dl_status s = dev_alloc(p, &p->d_hist, cap);
+    if (s) return s;
+    p->hist_cap = cap;
+  }
+  p->prm = *prm;
+  AgdDev st{};
+  const bool cont = prm->gamma_min > 0 && prm->gamma_min < prm->gamma0;
+  st.gamma = prm->gamma0;
+  st.gamma_prev = prm->gamma0;
+  st.eta = prm->init_step;
+  st.t = 0;
+  st.k = 1;
+  st.gamma0 = prm->gamma0;
+  st.gamma_min = cont ? prm->gamma_min : prm->gamma0;
+  st.gamma_ref = cont ? prm->gamma_min : prm->gamma0;
+  st.max_step = prm->max_step;
+  st.init_step = prm->init_step;
+  st.halve_every = std::max(prm->halve_every, 1);
+  st.continuation = cont ? 1 : 0;
+  st.hist_cap = cap;
+  CUDA_TRY(cudaMemcpyAsync(p->d_st, &st, sizeof(st), cudaMemcpyHostToDevice, p->stream));
+  for (double* q : {p->d_lam1, p->d_lam2, p->d_lam2_prev, p->d_G_prev})
+    CUDA_TRY(cudaMemsetAsync(q, 0, n * sizeof(double), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->d_mu, 0, n * sizeof(float), p->stream));
+  CUDA_TRY(launch_slack(p->d_mu, p->M, p->J, p->cmax, p->amax, p->d_slack + 1, p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->d_acc, 0, (n + 4) * sizeof(double), p->stream));
+  CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, 8 * sizeof(int32_t), p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));  // st is a stack object
+  p->agd_ready = true;
+  return DL_OK;
+}
+
+dl_status dl_agd_eval(dl_problem* p) {
+  if (!p || !p->agd_ready) {
+    set_error("dl_agd_eval: call dl_agd_init first");
+    return DL_ERR_STATE;
+  }
+  DeviceGuard guard(p->device);
+  return run_grad(p, p->d_mu, &p->d_st->gamma, 0.0, nullptr, false);
+}
+
+dl_status dl_agd_accumulator(dl_problem* p, double** acc, int64_t* n) {
+  if (!p || !acc || !n) {
+    set_error("dl_agd_accumulator: NULL argument");
+    return DL_ERR_INVALID;
+  }
+  *acc = p->d_acc;
+  *n = (int64_t)p->M * p->J + 4;
+  return DL_OK;
+}
+
+dl_status dl_dual_step(dl_problem* p) {
+  if (!p || !p->agd_ready) {
+    set_error("dl_dual_step: call dl_agd_init first");
+    return DL_ERR_STATE;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(launch_agd_step(step_args(p), p->stream));
+  return DL_OK;
+}
+
+dl_status dl_solve(dl_problem* p, int64_t iters) {
+  if (!p || !p->agd_ready) {
+    set_error("dl_solve: call dl_agd_init first");
+    return DL_ERR_STATE;
+  }
+  if (iters <= 0) return DL_OK;
+  DeviceGuard guard(p->device);
+  constexpr int kUnroll = 8;
+  if (!p->graph) {
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+    dl_status s = DL_OK;
+    for (int i = 0; i < kUnroll && s == DL_OK; ++i) s = enqueue_iteration(p);
+    cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+    if (s != DL_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    CUDA_TRY(e);
+    e = cudaGraphInstantiate(&p->graph, g, 0);
+    cudaGraphDestroy(g);
+    CUDA_TRY(e);
+    p->graph_iters = kUnroll;
+  }
+  int64_t full = iters / p->graph_iters, rem = iters % p->graph_iters;
+  for (int64_t i = 0; i < full; ++i) CUDA_TRY(cudaGraphLaunch(p->graph, p->stream));
+  for (int64_t i = 0; i < rem; ++i) DL_TRY(enqueue_iteration(p));
+  return DL_OK;
+}
+
+dl_status dl_agd_history(dl_problem* p, dl_iter_record* outr, int64_t cap, int64_t* count) {
+  if (!p || !p->agd_ready || !count) {
+    set_error("dl_agd_history: not initialised or NULL count");
+    return DL_ERR_STATE;
+  }
+  DeviceGuard guard(p->device);
+  AgdDev st;
+  CUDA_TRY(cudaMemcpyAsync(&st, p->d_st, sizeof(st), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  const int64_t avail = std::min(st.t, p->hist_cap);
+  *count = st.t;
+  if (outr && cap > 0) {
+    const int64_t n = std::min(avail, cap);
+    if (n > 0) CUDA_TRY(cudaMemcpy(outr, p->d_hist, n * sizeof(dl_iter_record), cudaMemcpyDeviceToHost));
+  }
+  return DL_OK;
+}
+
+dl_status dl_agd_dual(dl_problem* p, double* lam1_out, double* lam2_out) {
+  if (!p || !p->agd_ready) {
+    set_error("dl_agd_dual: call dl_agd_init first");
+    return DL_ERR_STATE;
+  }
+  DeviceGuard guard(p->device);
+  const int32_t n = p->M * p->J;
+  const double* D = p->prm.use_jacobi ? p->d_D : p->d_Dones;
+  double* outs[2] = {lam1_out, lam2_out};
+  const double* src[2] = {p->d_lam1, p->d_lam2};
+  for (int q = 0; q < 2; ++q) {
+    if (!outs[q]) continue;
+    cudaPointerAttributes at{};
+    bool dev = cudaPointerGetAttributes(&at, outs[q]) == cudaSuccess && at.type == cudaMemoryTypeDevice;
+    cudaGetLastError();
+    if (dev) {
+      CUDA_TRY(launch_scale_out(D, src[q], outs[q], n, p->stream));
+    } else {
+      CUDA_TRY(launch_scale_out(D, src[q], p->d_grad_out, n, p->stream));
+      CUDA_TRY(cudaMemcpyAsync(outs[q], p->d_grad_out, n * sizeof(double), cudaMemcpyDeviceToHost, p->stream));
+      CUDA_TRY(cudaStreamSynchronize(p->stream));
+    }
+  }
+  return DL_OK;
+}
+
+dl_status dl_comm_unique_id(void* id) {
+  if (!id) {
+    set_error("dl_comm_unique_id: NULL");
+    return DL_ERR_INVALID;
+  }
+  if (!load_nccl()) return DL_ERR_NCCL;
+  ncclUniqueId u;
+  if (g_nccl.GetUniqueId(&u) != 0) {
+    set_error("ncclGetUniqueId failed");
+    return DL_ERR_NCCL;
+  }
+  std::memcpy(id, &u, sizeof(u));
+  return DL_OK;
+}
+
+dl_status dl_comm_init(dl_problem* p, int32_t rank, int32_t world, const void* id) {
+  if (!p || !id || world < 1 || rank < 0 || rank >= world) {
+    set_error("dl_comm_init: bad arguments");
+    return DL_ERR_INVALID;
+  }
+  if (world == 1) return DL_OK;
+  if (!load_nccl()) return DL_ERR_NCCL;
+  DeviceGuard guard(p->device);
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t c = nullptr;
+  ncclResult_t r = g_nccl.CommInitRank(&c, world, u, rank);
+  if (r != 0) {
+    set_error(std::string("ncclCommInitRank: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+    return DL_ERR_NCCL;
+  }
+  if (p->graph) {
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+  }
+  p->comm = c;
+  p->rank = rank;
+  p->world = world;
+  return DL_OK;
+}
+
+dl_status dl_comm_allreduce(dl_problem* p, double* buf, int64_t n) {
+  if (!p || !buf || n < 0) {
+    set_error("dl_comm_allreduce: bad arguments");
+    return DL_ERR_INVALID;
+  }
+  if (!p->comm || n == 0) return DL_OK;
+  DeviceGuard guard(p->device);
+  ncclResult_t r = g_nccl.AllReduce(buf, buf, (size_t)n, kNcclFloat64, kNcclSum, p->comm, p->stream);
+  if (r != 0) {
+    set_error("ncclAllReduce failed");
+    return DL_ERR_NCCL;
+  }
+  return DL_OK;
+}
+
+dl_status dl_sync(dl_problem* p) {
+  if (!p) {
+    set_error("dl_sync: NULL");
+    return DL_ERR_INVALID;
+  }
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return DL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,876 @@
+// Fused dual-gradient pass (K1).
+//
+// One persistent CTA per SM (16 warps).  For every source block i:
+//   s_ij = c_ij + sum_k a_kij lambda_kj                 (reduced cost)
+//   y_ij = -s_ij / gamma_i,  gamma_i = gamma v_i^2
+//   x_i  = Pi_{C_i}(y_i) = clip(phi - d_ij, 0, u),  d_ij = (s_ij - min_j s_ij)/gamma_i,
+//          phi the threshold of the block polytope (R1, R7)
+//   acc[k*J + j] += a_kij x_ij   (fp64 red.global, only where x_ij > 0)
+//   acc[mJ+0] += c_ij x_ij, acc[mJ+1] += gamma_i/2 x_ij^2, acc[mJ+2] += [x_ij > 0]
+//
+// Work = the tile list of the layout (plan.cpp).
+//  Phase 1 (blocks >= 256 entries, buckets >= 9): multi-warp groups (16/8/4/2 warps for
+//   buckets >=12/11/10/9) read the block from global memory; d in an fp64 scratch.
+//  Phase 2 (short blocks): every warp pulls tiles independently; a tile's dest / c / a_k
+//   arrays arrive by cp.async.bulk (TMA bulk copy) into a per-warp double buffer with an
+//   mbarrier.  A tile's blocks are worked by groups of G = 1..32 lanes (G = 2^(t-3) for
+//   bucket t), <= 8 entries per lane.
+//   Fast filter: s is first formed in fp32 (one FMA per family) and only entries with
+//   s32 - min s32 <= gamma_i r + slack can have x > 0 on the simplex (active d < phi <= r),
+//   resp. s32 < slack on the box.  Those candidates alone are re-formed exactly in fp64
+//   (products of fp32 are exact in fp64) and the threshold is solved in fp64 (Michelot,
+//   one or two candidates per lane: shuffle reductions over the group).  Box-cut blocks
+//   and groups with more candidates take the generic exact path: fp64 d for every entry,
+//   safeguarded Newton on the piecewise-linear F(phi) = sum clip(phi - d, 0, u) with an
+//   Illinois-secant / bisection fallback.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace dl {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+#define kInfF __int_as_float(0x7f800000)
+#define kInfD __longlong_as_double(0x7ff0000000000000LL)
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- group reductions
+// Butterflies over aligned groups of G lanes (G a power of two <= 32): every lane of
+// a group ends with bitwise the same value (a+b == b+a in IEEE arithmetic).
+template <class T>
+__device__ __forceinline__ T gsum(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T gmin(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T gmax(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------- exact threshold solver
+// F(phi) = u nC + phi nM - sM with M = {phi-u < d < phi}, C = {d <= phi-u} (fp64).
+struct Sums {
+  double nM, sM, nC;
+};
+__device__ __forceinline__ double capsum(double u, double nC) { return nC > 0.0 ? u * nC : 0.0; }
+__device__ __forceinline__ double Fval(double phi, double u, const Sums& s) {
+  return capsum(u, s.nC) + phi * s.nM - s.sM;
+}
+
+struct Solver {
+  double lo, hi, Flo, Fhi, phi;
+  int side;   // last bracket end replaced: +1 hi, -1 lo (Illinois)
+  bool done;
+  bool free;  // theta = 0: the clamp alone is feasible, phi = phi_free
+};
+
+// Start at hi0 (F(hi0) >= r unless hi0 == phi_free); bracket [0, hi0] (F(0) = 0 <= r as d >= 0).
+__device__ __forceinline__ void solver_start(Solver& S, double r, double u, double phi_free, const Sums& s0,
+                                             double hi0) {
+  const double F = Fval(hi0, u, s0);
+  S.lo = 0.0;
+  S.Flo = 0.0;
+  S.hi = hi0;
+  S.Fhi = F;
+  S.phi = hi0;
+  S.side = 0;
+  S.done = false;
+  S.free = false;
+  if (hi0 == phi_free && F <= r) {
+    S.phi = phi_free;
+    S.done = true;
+    S.free = true;
+  } else if (F == r) {
+    S.done = true;
+  }
+}
+// Newton step from the partition at S.phi; falls back to Illinois secant / bisection.
+__device__ __forceinline__ double solver_candidate(Solver& S, double r, double u, const Sums& s) {
+  double cand = s.nM > 0.0 ? (r - capsum(u, s.nC) + s.sM) / s.nM : __longlong_as_double(0x7ff8000000000000LL);
+  if (!(cand > S.lo && cand < S.hi)) {
+    cand = S.Fhi > S.Flo ? S.lo + (r - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5 * (S.lo + S.hi);
+    if (!(cand > S.lo && cand < S.hi)) cand = 0.5 * (S.lo + S.hi);
+  }
+  if (cand == S.phi) S.done = true;
+  return cand;
+}
+__device__ __forceinline__ void solver_update(Solver& S, double r, double u, const Sums& s) {
+  const double F = Fval(S.phi, u, s);
+  if (F > r) {
+    S.hi = S.phi;
+    S.Fhi = F;
+    if (S.side == 1) S.Flo = r + 0.5 * (S.Flo - r);  // Illinois: lo retained twice
+    S.side = 1;
+  } else if (F < r) {
+    S.lo = S.phi;
+    S.Flo = F;
+    if (S.side == -1) S.Fhi = r + 0.5 * (S.Fhi - r);
+    S.side = -1;
+  } else {
+    S.done = true;
+  }
+  if (!(S.hi - S.lo > 4e-16 * fabs(S.hi))) S.done = true;
+}
+
+// ---------------------------------------------------------------- shared memory
+struct SmemHead {
+  uint64_t mbar[kWarps][2];
+  double red[2][kWarps][4];
+  int32_t slot[16];
+};
+static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
+
+template <int M, bool LAMS, bool WX>
+struct Ctx {
+  const GradArgs& p;
+  const float* lam_s;  // shared lambda (LAMS)
+  double gamma, invgamma;
+  double cx = 0.0, reg = 0.0;
+  float nx = 0.f;
+  __device__ Ctx(const GradArgs& pp, const float* ls, double g) : p(pp), lam_s(ls), gamma(g), invgamma(1.0 / g) {}
+
+  __device__ __forceinline__ float lam(int f, int j) const {
+    if constexpr (LAMS) return lam_s[f * p.J + j];
+    return __ldg(p.lam + (size_t)f * p.J + j);
+  }
+  // contribution of one positive x (fp64) to A x, the objective scalars and x_out
+  __device__ __forceinline__ void emit(int j, float cval, const float* av, double x, double vs, int b, int e) {
+#pragma unroll
+    for (int f = 0; f < M; ++f) atomicAdd(p.acc + (size_t)f * p.J + j, (double)av[f] * x);
+    cx += (double)cval * x;
+    reg += 0.5 * gamma * vs * x * x;
+    nx += 1.f;
+    if constexpr (WX) p.x_out[__ldg(p.orig_off + b) + e] = (float)x;
+  }
+};
+
+// ---------------------------------------------------------------- phase 1: big blocks
+struct BigGroup {
+  int gw, G, gtid, warp0, bar, lane, warp;
+  int rb = 0;
+  SmemHead* head;
+  __device__ __forceinline__ void sync() { named_bar(bar, G); }
+  // reduce up to 3 doubles with op (0 sum, 1 min, 2 max); deterministic order
+  template <int N>
+  __device__ __forceinline__ void reduce(double (&v)[N], int op) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      for (int o = 16; o > 0; o >>= 1) {
+        double w = __shfl_xor_sync(kFull, v[i], o);
+        v[i] = op == 0 ? v[i] + w : (op == 1 ? fmin(v[i], w) : fmax(v[i], w));
+      }
+    }
+    const int b = rb;
+    rb ^= 1;
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < N; ++i) head->red[b][warp][i] = v[i];
+    sync();
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double t = head->red[b][warp0][i];
+      for (int w = 1; w < gw; ++w) {
+        const double q = head->red[b][warp0 + w][i];
+        t = op == 0 ? t + q : (op == 1 ? fmin(t, q) : fmax(t, q));
+      }
+      v[i] = t;
+    }
+  }
+};
+
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ double score_global(const Ctx<M, LAMS, WX>& C, int64_t e) {
+  const GradArgs& p = C.p;
+  const int j = __ldg(p.dest + e);
+  double s = (double)__ldg(p.c + e);
+#pragma unroll
+  for (int f = 0; f < M; ++f) s = fma((double)__ldg(p.a + f * p.a_stride + e), (double)C.lam(f, j), s);
+  return s;
+}
+
+template <int M, bool LAMS, bool WX>
+__device__ void big_block(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, double* scr) {
+  const GradArgs& p = C.p;
+  const int len = tl.nnz;
+  const int64_t off = tl.off;
+  const int b = tl.b0;
+  const double r = p.r, u = p.u;
+  // pass 1: exact minimum reduced cost
+  double mn[1] = {DBL_MAX};
+#pragma unroll 4
+  for (int e = g.gtid; e < len; e += g.G) mn[0] = fmin(mn[0], score_global(C, off + e));
+  g.reduce(mn, 1);
+  const double smin = mn[0];
+  const double vs = p.vsq ? (double)__ldg(p.vsq + b) : 1.0;
+  const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + b) : C.invgamma;
+  const double phi_free = -smin * ginv;
+  // pass 2: d = (s - smin)/gamma_i into the scratch (own entries only)
+  double mx[1] = {-DBL_MAX};
+#pragma unroll 4
+  for (int e = g.gtid; e < len; e += g.G) {
+    const double d = (score_global(C, off + e) - smin) * ginv;
+    scr[e] = d;
+    mx[0] = fmax(mx[0], d);
+  }
+  double phi = phi_free;
+  bool free = true;
+  if (p.kind != DL_PROJ_BOX) {
+    if (p.kind == DL_PROJ_BOXCUT) g.reduce(mx, 2);
+    auto eval = [&](double ph) {
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int e = g.gtid; e < len; e += g.G) {
+        const double d = scr[e];
+        if (d < ph) {
+          if (d > ph - u) {
+            v[0] += 1.0;
+            v[1] += d;
+          } else {
+            v[2] += 1.0;
+          }
+        }
+      }
+      g.reduce(v, 0);
+      return Sums{v[0], v[1], v[2]};
+    };
+    const double hi0 = p.kind == DL_PROJ_SIMPLEX ? fmin(phi_free, r) : fmin(phi_free, mx[0] + u);
+    Solver S;
+    Sums cur = eval(hi0);
+    solver_start(S, r, u, phi_free, cur, hi0);
+    for (int it = 0; it < 200 && !S.done; ++it) {
+      const double cand = solver_candidate(S, r, u, cur);
+      if (S.done) break;
+      S.phi = cand;
+      cur = eval(S.phi);
+      solver_update(S, r, u, cur);
+    }
+    phi = S.phi;
+    free = S.free;
+  }
+  for (int e = g.gtid; e < len; e += g.G) {
+    const double d = scr[e];
+    const double x = free ? fmin(fmax(phi_free - d, 0.0), u) : fmin(fmax(phi - d, 0.0), u);
+    if (x > 0.0) {
+      const int j = __ldg(p.dest + off + e);
+      float av[M];
+#pragma unroll
+      for (int f = 0; f < M; ++f) av[f] = __ldg(p.a + f * p.a_stride + off + e);
+      C.emit(j, __ldg(p.c + off + e), av, x, vs, b, e);
+    }
+  }
+  g.sync();  // scratch reuse by the next block of this group
+}
+
+// ---------------------------------------------------------------- phase 2: small tiles
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ double score_smem(const Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+                                             const float* sa, int cap, int ee) {
+  const int j = sd[ee];
+  double s = (double)sc[ee];
+#pragma unroll
+  for (int f = 0; f < M; ++f) s = fma((double)sa[f * cap + ee], (double)C.lam(f, j), s);
+  return s;
+}
+
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ void emit_smem(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc, const float* sa,
+                                          int cap, int ee, double x, double vs, int b, int e) {
+  float av[M];
+#pragma unroll
+  for (int f = 0; f < M; ++f) av[f] = sa[f * cap + ee];
+  C.emit(sd[ee], sc[ee], av, x, vs, b, e);
+}
+
+// Compile-time group reductions (G lanes, aligned groups inside the warp).
+template <int G, class T>
+__device__ __forceinline__ T tsum(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <int G, class T>
+__device__ __forceinline__ T tmin(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+template <int G, class T>
+__device__ __forceinline__ T tmax(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+// number of set predicates over the group's lanes (one vote)
+template <int G>
+__device__ __forceinline__ int tcount(bool pred, uint32_t gmask) {
+  return __popc(__ballot_sync(kFull, pred) & gmask);
+}
+
+// fp32 threshold solver state for the generic small path (partition only; the final
+// threshold is recomputed in fp64 from the partition).
+struct SolverF {
+  float lo, hi, Flo, Fhi, phi;
+  int side;
+  bool done, free;
+};
+struct SumsF {
+  float nM, sM, nC;
+};
+__device__ __forceinline__ float capsumf(float u, float nC) { return nC > 0.f ? u * nC : 0.f; }
+
+// Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
+template <int M, bool LAMS, bool WX, int LG, int E>
+__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane, float slack, int relA,
+                           int relB) {
+  constexpr int G = 1 << LG;
+  constexpr int NG = 32 >> LG;
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;  // family f at sa + f*cap
+  const int gi = lane >> LG, q = lane & (G - 1);
+  const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
+  const int nrounds = (tl.nb + NG - 1) / NG;
+  const double r = p.r, u = p.u;
+  const float rf = p.r, uf = p.u;
+  const int kind = p.kind;
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const int bb = rd * NG + gi;
+    const bool active = bb < tl.nb;
+    const int b = tl.b0 + bb;
+    // block bounds: relative offsets of the tile's blocks were prefetched into relA (blocks
+    // 0..31) / relB (32..63) of the lanes; tiles with more blocks read them directly
+    int start, end;
+    if (tl.nb < 63) {
+      const int ia = bb, ib = bb + 1;
+      const int sa0 = __shfl_sync(kFull, relA, ia & 31), sb0 = __shfl_sync(kFull, relB, ia & 31);
+      const int sa1 = __shfl_sync(kFull, relA, ib & 31), sb1 = __shfl_sync(kFull, relB, ib & 31);
+      start = ia < 32 ? sa0 : sb0;
+      end = ib < 32 ? sa1 : sb1;
+    } else {
+      start = active ? (int)__ldg(p.blk_rel + b) : 0;
+      end = active ? (bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz) : 0;
+    }
+    if (!active) start = end = 0;
+    const int len = end - start;
+    double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
+    if (p.vsq) {
+      if (active) {
+        vs = (double)__ldg(p.vsq + b);
+        ginv = C.invgamma * (double)__ldg(p.vinv + b);
+      }
+    }
+    // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family).
+    // Reads past the block end stay inside the stage buffers (tail padding); their dest is
+    // clamped to [0, J) and their s32 replaced by +inf.
+    const int32_t* sdp = sd + start + q;
+    const float* scp = sc + start + q;
+    const float* sap = sa + start + q;
+    const int lim = len - q;  // slot k of this lane is inside the block iff k*G < lim
+    float s32[E];
+    float lmin = kInfF;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int j = (int)min((unsigned)sdp[k * G], Jm1);
+      float sv = scp[k * G];
+#pragma unroll
+      for (int f = 0; f < M; ++f) sv = fmaf(sap[f * cap + k * G], C.lam(f, j), sv);
+      s32[k] = k * G < lim ? sv : kInfF;
+      lmin = fminf(lmin, s32[k]);
+    }
+    // ---- candidates: entries that can have x > 0.  |fl32(s) - s| <= M 2^-24 B per entry with
+    // B the launch-wide magnitude bound; `slack` = 2^-19 (M+1) B covers two such errors 8x over.
+    uint32_t cm = 0;
+    float ref = 0.f;
+    if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= slack) cm |= 1u << k;
+    } else if (kind == DL_PROJ_SIMPLEX) {  // active d < phi <= r  =>  s - s_min < gamma_i r
+      ref = tmin<G>(lmin);
+      const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= T) cm |= 1u << k;
+    } else {  // box-cut: active d < phi <= d_(K) + u, K = ceil(r/u): window above the K-th smallest s
+      const int K = (int)ceil(r / u);
+      float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
+      uint32_t excl = 0;
+      bool sat = !active;
+      if (K <= 8) {
+        for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
+          float ml = kInfF;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
+          const float m = tmin<G>(ml);
+          float c = 0.f;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u) && s32[k] == m) {
+              c += 1.f;
+              excl |= 1u << k;
+            }
+          c = tsum<G>(c);
+          if (!sat) {
+            if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
+              sat = true;
+            } else {
+              cnt += c;
+              sk = m;
+              if (cnt >= (float)K) sat = true;
+            }
+          }
+        }
+      }
+      ref = sat ? sk : 0.f;
+      if (sat) {
+        const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] <= T) cm |= 1u << k;
+      } else {  // K > 8: every entry is a candidate
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] < kInfF) cm |= 1u << k;
+      }
+    }
+    if (!active) cm = 0;
+    if (kind == DL_PROJ_BOX) {  // no coupling inside the block: x = clip(-s/gamma_i, 0, u) per entry
+      while (cm) {
+        const int k = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const int e = q + k * G, ee = start + e;
+        const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), u);
+        if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ee, x, vs, b, e);
+      }
+      continue;
+    }
+    const double refd = (double)ref;
+    const int nc = __popc(cm);
+    if (kind == DL_PROJ_SIMPLEX && __all_sync(kFull, nc <= 3)) {
+      // ---- simplex, <= 3 candidates per lane: exact fp64 Michelot on the candidates only
+      double d0 = kInfD, d1 = kInfD, d2 = kInfD;
+      int e0 = -1, e1 = -1, e2 = -1;
+      uint32_t m = cm;
+      if (m) {
+        e0 = q + (__ffs(m) - 1) * G;
+        m &= m - 1;
+        d0 = (score_smem(C, sd, sc, sa, cap, start + e0) - refd) * ginv;
+        if (m) {
+          e1 = q + (__ffs(m) - 1) * G;
+          m &= m - 1;
+          d1 = (score_smem(C, sd, sc, sa, cap, start + e1) - refd) * ginv;
+          if (m) {
+            e2 = q + (__ffs(m) - 1) * G;
+            d2 = (score_smem(C, sd, sc, sa, cap, start + e2) - refd) * ginv;
+          }
+        }
+      }
+      const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
+      const int T = tcount<G>(e0 >= 0, gmask) + tcount<G>(e1 >= 0, gmask) + tcount<G>(e2 >= 0, gmask);
+      // |d_min| <= slack/gamma_i (ref = fl32 minimum), so F(r + slack/gamma_i) >= r
+      double phi = fmin(phi_free, r + (double)slack * ginv);
+      bool free = false, done = !active || T <= 1;
+      int cprev = -1;
+      bool first = true;
+      while (__any_sync(kFull, !done)) {
+        const bool i0 = d0 < phi, i1 = d1 < phi, i2 = d2 < phi;
+        const int cnt = tcount<G>(i0, gmask) + tcount<G>(i1, gmask) + tcount<G>(i2, gmask);
+        const double sm = tsum<G>((i0 ? d0 : 0.0) + (i1 ? d1 : 0.0) + (i2 ? d2 : 0.0));
+        if (!done) {
+          if (first && phi == phi_free && phi * cnt - sm <= r) {
+            free = true;
+            done = true;
+          } else {
+            phi = (r + sm) / cnt;  // Michelot: exact threshold of the current set
+            done = cnt == cprev;   // set unchanged => phi is the root
+            cprev = cnt;
+          }
+        }
+        first = false;
+      }
+      if (active) {
+        if (T == 1) {  // a single candidate: x = clip(-s/gamma_i, 0, r)
+          if (e0 >= 0) {
+            const double x = fmin(fmax(phi_free - d0, 0.0), r);
+            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
+          }
+        } else {
+          const double ph = free ? phi_free : phi;
+          if (e0 >= 0) {
+            const double x = fmax(ph - d0, 0.0);
+            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
+          }
+          if (e1 >= 0) {
+            const double x = fmax(ph - d1, 0.0);
+            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e1, x, vs, b, e1);
+          }
+          if (e2 >= 0) {
+            const double x = fmax(ph - d2, 0.0);
+            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e2, x, vs, b, e2);
+          }
+        }
+      }
+      continue;
+    }
+    // ---- generic path (box-cut, or > 3 candidates in a lane): exact s of the candidates,
+    // d = fl32((s - ref)/gamma_i) with ref = min s (simplex) or the K-th smallest s (box-cut), so
+    // every entry near a breakpoint is O(max(r, u)) in this frame; safeguarded Newton in fp32
+    // finds the partition, the threshold is then recomputed in fp64 from it.
+    float d[E];
+    float dmax = -kInfF, dmn = kInfF;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      d[k] = kInfF;
+      if (cm >> k & 1u) {
+        d[k] = (float)((score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv);
+        dmax = fmaxf(dmax, d[k]);
+        dmn = fminf(dmn, d[k]);
+      }
+    }
+    dmn = tmin<G>(dmn);
+    const double phi_free64 = -refd * ginv;
+    const float phi_free = (float)fmax(fmin(phi_free64, 1e30), -1e30);
+    auto local = [&](float ph) {
+      SumsF s{0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (d[k] < ph) {
+          if (d[k] > ph - uf) {
+            s.nM += 1.f;
+            s.sM += d[k];
+          } else {
+            s.nC += 1.f;
+          }
+        }
+      }
+      s.nM = tsum<G>(s.nM);
+      s.sM = tsum<G>(s.sM);
+      s.nC = tsum<G>(s.nC);
+      return s;
+    };
+    float hi0 = kind == DL_PROJ_SIMPLEX ? fminf(phi_free, dmn + rf) : fminf(phi_free, tmax<G>(dmax) + uf);
+    SolverF S;
+    S.done = true;
+    S.free = true;
+    S.phi = phi_free;
+    S.lo = S.hi = S.Flo = S.Fhi = 0.f;
+    S.side = 0;
+    SumsF cur = local(hi0);
+    if (active) {
+      const float F = capsumf(uf, cur.nC) + hi0 * cur.nM - cur.sM;
+      S.lo = dmn;  // F(d_min) = 0
+      S.Flo = 0.f;
+      S.hi = hi0;
+      S.Fhi = F;
+      S.phi = hi0;
+      S.free = hi0 == phi_free && F <= rf;
+      S.done = S.free || F == rf;
+    }
+    for (int it = 0; it < 200 && __any_sync(kFull, !S.done); ++it) {
+      if (!S.done) {
+        float cand = cur.nM > 0.f ? (rf - capsumf(uf, cur.nC) + cur.sM) / cur.nM : __int_as_float(0x7fc00000);
+        if (!(cand > S.lo && cand < S.hi)) {
+          cand = S.Fhi > S.Flo ? S.lo + (rf - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5f * (S.lo + S.hi);
+          if (!(cand > S.lo && cand < S.hi)) cand = 0.5f * (S.lo + S.hi);
+        }
+        if (cand == S.phi) S.done = true;
+        else S.phi = cand;
+      }
+      const bool want = !S.done;
+      if (!__any_sync(kFull, want)) break;
+      cur = local(S.phi);
+      if (want) {
+        const float F = capsumf(uf, cur.nC) + S.phi * cur.nM - cur.sM;
+        if (F > rf) {
+          S.hi = S.phi;
+          S.Fhi = F;
+          if (S.side == 1) S.Flo = rf + 0.5f * (S.Flo - rf);
+          S.side = 1;
+        } else if (F < rf) {
+          S.lo = S.phi;
+          S.Flo = F;
+          if (S.side == -1) S.Fhi = rf + 0.5f * (S.Fhi - rf);
+          S.side = -1;
+        } else {
+          S.done = true;
+        }
+        if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
+      }
+    }
+    // exact threshold from the partition at S.phi: phi = (r - u|C| + sum_M d)/|M|
+    const float ph32 = S.phi;
+    double sM = 0.0;
+    float nM = 0.f, nC = 0.f;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      if (d[k] < ph32) {
+        if (d[k] > ph32 - uf) {
+          nM += 1.f;
+          sM += (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
+        } else {
+          nC += 1.f;
+        }
+      }
+    }
+    nM = tsum<G>(nM);
+    nC = tsum<G>(nC);
+    sM = tsum<G>(sM);
+    if (!active) continue;
+    const double ph = S.free ? phi_free64
+                             : (nM > 0.f ? (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM : (double)ph32);
+    const float margin = 1e-5f * fmaxf(fabsf(ph32), 1.f);
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      if ((cm >> k & 1u) && d[k] < ph32 + margin) {
+        const int e = q + k * G;
+        const double dd = (score_smem(C, sd, sc, sa, cap, start + e) - refd) * ginv;
+        const double x = fmin(fmax(ph - dd, 0.0), u);
+        if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e, x, vs, b, e);
+      }
+    }
+  }
+}
+
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
+                                               float slack, int relA, int relB) {
+  switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
+    case 1:
+    case 2:
+    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    case 6: small_tile<M, LAMS, WX, 3, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    case 7: small_tile<M, LAMS, WX, 4, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    default: small_tile<M, LAMS, WX, 5, 8>(C, tl, stage, lane, slack, relA, relB); break;
+  }
+}
+
+template <int M, bool LAMS, bool WX>
+__global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const GradArgs p) {
+  extern __shared__ __align__(128) char smem[];
+  SmemHead* head = reinterpret_cast<SmemHead*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* after_head = smem + 2048;
+  float* lam_s = nullptr;
+  size_t lam_bytes = 0;
+  if constexpr (LAMS) {
+    lam_s = reinterpret_cast<float*>(after_head);
+    lam_bytes = ((size_t)M * p.J * 4 + 127) / 128 * 128;
+    const int n = M * p.J;
+    for (int i = threadIdx.x; i < n; i += kThreads) lam_s[i] = __ldg(p.lam + i);
+  }
+  char* tilebuf = after_head + lam_bytes;
+  const uint32_t stage_bytes = (uint32_t)p.tile_cap * (8u + 4u * M);
+  if (lane == 0) {
+    mbar_init(&head->mbar[warp][0], 1);
+    mbar_init(&head->mbar[warp][1], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
+  const float slack = *p.slack;  // fl32 error bound of s (see small_tile), per launch
+  Ctx<M, LAMS, WX> C(p, lam_s, gamma);
+
+  // ---- phase 1: big blocks, groups of 16 / 8 / 4 / 2 warps; barrier ids unique per group
+  for (int ph = 0; ph < kNumBigPhases; ++ph) {
+    if (p.ph_begin[ph] == p.ph_begin[ph + 1]) continue;
+    BigGroup g;
+    g.gw = 16 >> ph;
+    g.G = g.gw * 32;
+    const int grp = warp / g.gw;
+    g.warp0 = grp * g.gw;
+    g.gtid = (warp - g.warp0) * 32 + lane;
+    g.bar = (1 << ph) + grp;  // phase 0: 1, phase 1: 2-3, phase 2: 4-7, phase 3: 8-15
+    g.lane = lane;
+    g.warp = warp;
+    g.head = head;
+    // scratch: this group's warps' tile buffers (doubles), else a global slice
+    double* scr_smem = reinterpret_cast<double*>(tilebuf + (size_t)g.warp0 * 2 * stage_bytes);
+    const int scr_cap = (int)((size_t)g.gw * 2 * stage_bytes / 8);
+    for (;;) {
+      if (g.gtid == 0) head->slot[g.bar] = atomicAdd(p.ctr + ph, 1) + p.ph_begin[ph];
+      g.sync();
+      const int ti = head->slot[g.bar];
+      if (ti >= p.ph_begin[ph + 1]) break;
+      const Tile tl = p.tiles[ti];
+      double* scr = tl.nnz <= scr_cap ? scr_smem : p.gscratch + (size_t)blockIdx.x * p.gscratch_per_cta;
+      big_block<M, LAMS, WX>(C, g, tl, scr);
+    }
+  }
+
+  // ---- phase 2: small tiles, each warp on its own double-buffered TMA stream.  Tiles are
+  // claimed in chunks of kChunk (one atomic per chunk, claimed a chunk ahead); tile
+  // descriptors are loaded two tiles ahead and block offsets one tile ahead, so neither the
+  // atomic nor the descriptor loads sit on the critical path.
+  {
+    constexpr int kChunk = 4;
+    const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
+    char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
+    uint64_t* bars = head->mbar[warp];
+    auto grab = [&]() {
+      int ti = 0;
+      if (lane == 0) ti = atomicAdd(p.ctr + kNumBigPhases, 1) * kChunk + s_begin;
+      return __shfl_sync(kFull, ti, 0);
+    };
+    auto load_desc = [&](int ti) {
+      Tile t{};
+      t.nb = 0;
+      if (ti < s_end) t = p.tiles[ti];
+      return t;
+    };
+    auto load_rel = [&](const Tile& t, int& ra, int& rb) {
+      ra = rb = 0;
+      if (t.nb > 0 && t.nb < 63) {
+        const int i0 = lane, i1 = lane + 32;
+        ra = i0 < t.nb ? (int)__ldg(p.blk_rel + t.b0 + i0) : (i0 == t.nb ? t.nnz : 0);
+        rb = i1 < t.nb ? (int)__ldg(p.blk_rel + t.b0 + i1) : (i1 == t.nb ? t.nnz : 0);
+      }
+    };
+    auto issue = [&](const Tile& t, int st) {
+      if (lane == 0) {
+        const uint32_t n4 = (uint32_t)((t.nnz + kAlign - 1) / kAlign * kAlign);
+        const uint32_t bytes = n4 * 4u;
+        char* dst = mybuf + (size_t)st * stage_bytes;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[st], bytes * (2u + M));
+        tma_bulk_g2s(dst, p.dest + t.off, bytes, &bars[st]);
+        tma_bulk_g2s(dst + (size_t)p.tile_cap * 4, p.c + t.off, bytes, &bars[st]);
+#pragma unroll
+        for (int f = 0; f < M; ++f)
+          tma_bulk_g2s(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st]);
+      }
+    };
+    int cb = grab(), nbase = grab();  // current / next chunk base
+    int pos = 0;
+    auto ahead = [&](int k) {  // index of the tile k places after the current one
+      const int q2 = pos + k;
+      const int ti = q2 < kChunk ? cb + q2 : nbase + (q2 - kChunk);
+      const int limit = q2 < kChunk ? cb + kChunk : nbase + kChunk;
+      return (ti < s_end && ti < limit) ? ti : s_end;
+    };
+    uint32_t phase[2] = {0u, 0u};
+    int st = 0;
+    int cur = cb < s_end ? cb : s_end;
+    Tile tcur = load_desc(cur);
+    Tile tn1 = load_desc(ahead(1));
+    int relA, relB;
+    load_rel(tcur, relA, relB);
+    if (cur < s_end) issue(tcur, 0);
+    while (cur < s_end) {
+      const int n1 = ahead(1);
+      if (n1 < s_end) issue(tn1, st ^ 1);
+      const Tile tn2 = load_desc(ahead(2));
+      int nA, nB;
+      load_rel(tn1, nA, nB);
+      mbar_wait(&bars[st], phase[st]);
+      phase[st] ^= 1u;
+      small_dispatch<M, LAMS, WX>(C, tcur, mybuf + (size_t)st * stage_bytes, lane, slack, relA, relB);
+      __syncwarp();
+      // advance
+      if (++pos == kChunk) {
+        pos = 0;
+        cb = nbase;
+        nbase = cb < s_end ? grab() : s_end;
+      }
+      cur = n1;
+      tcur = tn1;
+      tn1 = tn2;
+      relA = nA;
+      relB = nB;
+      st ^= 1;
+    }
+  }
+
+  // ---- objective scalars: warp reduce, one fp64 atomic per warp
+  double cx = C.cx, rg = C.reg;
+  float nx = C.nx;
+  for (int o = 16; o > 0; o >>= 1) {
+    cx += __shfl_xor_sync(kFull, cx, o);
+    rg += __shfl_xor_sync(kFull, rg, o);
+    nx += __shfl_xor_sync(kFull, nx, o);
+  }
+  if (lane == 0) {
+    const size_t n = (size_t)M * p.J;
+    atomicAdd(p.acc + n + 0, cx);
+    atomicAdd(p.acc + n + 1, rg);
+    atomicAdd(p.acc + n + 2, (double)nx);
+  }
+}
+
+template <int M, bool LAMS, bool WX>
+cudaError_t launch_t(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  auto k = fused_grad_kernel<M, LAMS, WX>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<ctas, kThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  const bool wx = a.x_out != nullptr;
+  if (a.lam_smem) return wx ? launch_t<M, true, true>(a, ctas, smem, s) : launch_t<M, true, false>(a, ctas, smem, s);
+  return wx ? launch_t<M, false, true>(a, ctas, smem, s) : launch_t<M, false, false>(a, ctas, smem, s);
+}
+
+}  // namespace
+
+cudaError_t launch_fused_grad(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  switch (a.m) {
+    case 1: return launch_m<1>(a, ctas, smem, s);
+    case 2: return launch_m<2>(a, ctas, smem, s);
+    case 3: return launch_m<3>(a, ctas, smem, s);
+    case 4: return launch_m<4>(a, ctas, smem, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dl

@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same
+seeded inputs.  Tolerances (R12, north_star "1e-5 relative"):
+  |grad_gpu - grad_orc|_j <= 1e-5 ((A|x|)_j + |b_j|) + 1e-12
+  |g_gpu - g_orc|         <= 1e-5 (|c|^T x + gamma/2 x^T D_v^2 x + |mu|^T (A x + |b|))
+  |x_gpu - x_orc|         <= 2e-6 (x in [0, max(r, u)])
+Layout (buckets, permutation, offsets, tiles) is compared bit for bit.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from oracle.dual import BOX, BOXCUT, SIMPLEX, Problem, apply_A, dual_eval, row_sqnorms  # noqa: E402
+from oracle.layout import tile_plan  # noqa: E402
+from paper_2603_04621_b200 import MatchingProblem  # noqa: E402
+from synth.matching import GenConfig, generate  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def make(cfg, kind=SIMPLEX, r=1.0, u=1.0, v=None):
+    inst = generate(cfg)
+    gp = MatchingProblem.from_instance(inst, kind=kind, r=r, u=u, v=v)
+    P = Problem.from_instance(inst, kind=kind, r=r, u=(np.inf if kind == SIMPLEX else u), v=v)
+    return inst, gp, P
+
+
+def rand_lambda(rng, n, scale):
+    return (rng.exponential(scale, n) * (rng.random(n) < 0.8)).astype(np.float32)
+
+
+def check_grad(gp, P, lam32, gamma, x_check=True):
+    lam_t = torch.from_numpy(lam32).to(DEV)
+    grad, obj = gp.dual_grad(lam_t, gamma)
+    torch.cuda.synchronize()
+    grad, obj = grad.cpu().numpy(), obj.cpu().numpy()
+    lam = lam32.astype(np.float64)
+    ev = dual_eval(P, lam, gamma)
+    absAx = apply_A(P, np.abs(ev.x))
+    tol = 1e-5 * (absAx + np.abs(P.b)) + 1e-12
+    err = np.abs(grad - ev.grad)
+    assert np.all(err <= tol), (np.max(err / tol), np.argmax(err / tol))
+    gscale = float(np.abs(P.c) @ np.abs(ev.x)) + abs(ev.reg) + float(np.abs(lam) @ (absAx + np.abs(P.b)))
+    assert abs(obj[0] - ev.g) <= 1e-5 * gscale + 1e-12, (obj[0], ev.g)
+    assert abs(obj[1] - ev.cx) <= 1e-5 * (float(np.abs(P.c) @ np.abs(ev.x)) + 1e-12)
+    assert abs(obj[2] - ev.reg) <= 1e-5 * abs(ev.reg) + 1e-12
+    assert obj[3] == pytest.approx(np.count_nonzero(ev.x > 0), abs=max(3, 1e-3 * P.nnz))
+    if x_check:
+        x = gp.primal(lam_t, gamma)
+        torch.cuda.synchronize()
+        np.testing.assert_allclose(x.cpu().numpy(), ev.x, atol=2e-6, rtol=0)
+    return ev
+
+
+CASES = {
+    # name: (GenConfig, kind, r, u)
+    "poisson_simplex": (GenConfig(num_sources=3000, num_dests=400, nnz_per_source=100, seed=21), SIMPLEX, 1.0, 1.0),
+    "tiny_simplex": (GenConfig(num_sources=1000, num_dests=50, nnz_per_source=10, seed=1), SIMPLEX, 1.0, 1.0),
+    "powerlaw_simplex": (GenConfig(num_sources=2500, num_dests=20000, length_law="powerlaw", max_len=9000,
+                                   powerlaw_alpha=1.6, seed=22), SIMPLEX, 1.0, 1.0),
+    "boxcut_m2": (GenConfig(num_sources=2000, num_dests=300, nnz_per_source=60, num_families=2, seed=23),
+                  BOXCUT, 3.0, 1.0),
+    "boxcut_powerlaw": (GenConfig(num_sources=1500, num_dests=20000, length_law="powerlaw", max_len=6000,
+                                  powerlaw_alpha=1.5, seed=24), BOXCUT, 4.0, 0.6),
+    "box_m3": (GenConfig(num_sources=1500, num_dests=200, nnz_per_source=30, num_families=3, seed=25), BOX, 1.0, 0.5),
+    "bigJ_lambda_global": (GenConfig(num_sources=1500, num_dests=60000, nnz_per_source=40, seed=26),
+                           SIMPLEX, 2.0, 1.0),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_dual_grad_matches_oracle(name):
+    cfg, kind, r, u = CASES[name]
+    inst, gp, P = make(cfg, kind, r, u)
+    rng = np.random.default_rng(hash(name) % 2**32)
+    n = gp.n
+    for gamma in (0.01, 0.16, 1.0):
+        check_grad(gp, P, np.zeros(n, np.float32), gamma)
+        check_grad(gp, P, rand_lambda(rng, n, 2.0 / max(1.0, np.sqrt(inst.nnz / inst.num_dests))), gamma)
+    check_grad(gp, P, rand_lambda(rng, n, 50.0), 0.05)     # large duals: most x = 0
+    gp.close()
+
+
+def test_primal_scaling_matches_oracle():
+    cfg = GenConfig(num_sources=2000, num_dests=300, nnz_per_source=80, seed=27)
+    rng = np.random.default_rng(5)
+    v = rng.uniform(0.3, 3.0, cfg.num_sources).astype(np.float32)
+    for kind, r, u in ((SIMPLEX, 1.0, 1.0), (BOXCUT, 2.0, 0.7)):
+        inst, gp, P = make(cfg, kind, r, u, v=v)
+        for gamma in (0.02, 0.3):
+            check_grad(gp, P, rand_lambda(rng, gp.n, 0.1), gamma)
+        gp.close()
+
+
+def test_layout_bit_exact():
+    cfg = GenConfig(num_sources=4000, num_dests=20000, length_law="powerlaw", max_len=9000, powerlaw_alpha=1.7,
+                    seed=28)
+    inst = generate(cfg)
+    lens = np.diff(inst.row_ptr)
+    lens[::37] = 0  # empty blocks
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    keep = np.concatenate([np.arange(inst.row_ptr[i], inst.row_ptr[i] + lens[i]) for i in range(lens.size)])
+    dest, c, a = inst.dest[keep], inst.c[keep], inst.a[:, keep]
+    gp = MatchingProblem(rp, dest, a, c, inst.b, inst.num_dests)
+    perm, off, tiles = gp.layout()
+    operm, ooff, otiles, ototal = tile_plan(lens, gp.info["tile_cap"])
+    np.testing.assert_array_equal(perm, operm)
+    np.testing.assert_array_equal(off, ooff)
+    np.testing.assert_array_equal(tiles, np.array(otiles).reshape(-1, 5))
+    assert gp.info["nnz_layout"] == ototal
+    ld, lc, la = gp.layout_data()
+    for b in range(0, perm.size, 7):
+        i = perm[b]
+        sl = slice(rp[i], rp[i + 1])
+        o = slice(off[b], off[b] + lens[i])
+        np.testing.assert_array_equal(ld[o], dest[sl])
+        np.testing.assert_array_equal(lc[o], c[sl])
+        np.testing.assert_array_equal(la[:, o], a[:, sl])
+    gp.close()
+
+
+def test_row_sqnorms_match_oracle():
+    cfg = GenConfig(num_sources=3000, num_dests=500, nnz_per_source=40, num_families=2, seed=29)
+    inst, gp, P = make(cfg)
+    got = gp.row_sqnorms()
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(got.cpu().numpy(), row_sqnorms(P), rtol=1e-12, atol=0)
+    gp.close()
+
+
+def test_host_entry_equals_device_entry():
+    cfg = GenConfig(num_sources=2000, num_dests=300, nnz_per_source=50, seed=30)
+    inst, gp, P = make(cfg)
+    lam = rand_lambda(np.random.default_rng(1), gp.n, 0.2)
+    g_d, o_d = gp.dual_grad(torch.from_numpy(lam).to(DEV), 0.05)
+    torch.cuda.synchronize()
+    lam_h = torch.from_numpy(lam).pin_memory()
+    g_h = torch.zeros(gp.n, dtype=torch.float64).pin_memory()
+    o_h = torch.zeros(4, dtype=torch.float64).pin_memory()
+    gp.dual_grad_host(lam_h, 0.05, g_h, o_h)
+    np.testing.assert_allclose(g_h.numpy(), g_d.cpu().numpy(), rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(o_h.numpy()[1:], o_d.cpu().numpy()[1:], rtol=1e-12)
+    gp.close()
+
+
+def test_edge_cases():
+    # all blocks of length 1, J = 1, and an empty problem
+    for cfg in (GenConfig(num_sources=500, num_dests=1, nnz_per_source=3, seed=31),
+                GenConfig(num_sources=800, num_dests=3000, nnz_per_source=1.0, seed=32)):
+        inst, gp, P = make(cfg)
+        check_grad(gp, P, np.zeros(gp.n, np.float32), 0.1)
+        check_grad(gp, P, rand_lambda(np.random.default_rng(2), gp.n, 1.0), 0.1)
+        gp.close()
+    gp = MatchingProblem(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros((1, 0), np.float32),
+                         np.zeros(0, np.float32), np.ones(4, np.float32), 4)
+    grad, obj = gp.dual_grad(torch.full((4,), 0.5, device=DEV), 0.1)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(grad.cpu().numpy(), -np.ones(4))
+    assert obj.cpu().numpy()[0] == -2.0
+    gp.close()
