@@ -73,6 +73,7 @@ struct dl_problem {
   float *d_c = nullptr, *d_a = nullptr, *d_b = nullptr, *d_vsq = nullptr, *d_vinv = nullptr;
   Tile* d_tiles = nullptr;
   uint16_t* d_blk_rel = nullptr;
+  uint16_t* d_rel_pool = nullptr;
   int64_t* d_orig_off = nullptr;
   double* d_gscratch = nullptr;
   int64_t gscratch_per_cta = 0;
@@ -176,6 +177,7 @@ GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   a.tiles = p->d_tiles;
   for (int i = 0; i < kNumBigPhases + 2; ++i) a.ph_begin[i] = p->plan.ph_begin[i];
   a.blk_rel = p->d_blk_rel;
+  a.rel_pool = p->d_rel_pool;
   a.vsq = p->d_vsq;
   a.vinv = p->d_vinv;
   a.orig_off = p->d_orig_off;
@@ -349,7 +351,7 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
   dl_status s;
   if ((s = dev_alloc(p, &p->d_dest, p->a_stride)) || (s = dev_alloc(p, &p->d_c, p->a_stride)) ||
       (s = dev_alloc(p, &p->d_a, (size_t)p->a_stride * p->M)) || (s = dev_alloc(p, &p->d_b, MJ)) ||
-      (s = dev_alloc(p, &p->d_tiles, nt)) || (s = dev_alloc(p, &p->d_blk_rel, nb)) ||
+      (s = dev_alloc(p, &p->d_tiles, nt + 8)) || (s = dev_alloc(p, &p->d_blk_rel, nb)) ||
       (s = dev_alloc(p, &p->d_orig_off, nb)) || (s = dev_alloc(p, &p->d_acc, MJ + 4)) ||
       (s = dev_alloc(p, &p->d_ctr, 8)) || (s = dev_alloc(p, &p->d_D, MJ)) || (s = dev_alloc(p, &p->d_Dones, MJ)) ||
       (s = dev_alloc(p, &p->d_lam_in, MJ)) || (s = dev_alloc(p, &p->d_grad_out, MJ)) ||
@@ -370,15 +372,28 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
   // host -> device plan arrays
   std::vector<uint16_t> rel((size_t)nb, 0);
   std::vector<int64_t> orig((size_t)nb, 0);
-  for (const Tile& tl : P.tiles)
+  std::vector<uint16_t> pool;
+  for (Tile& tl : p->plan.tiles) {
     for (int q = 0; q < tl.nb; ++q) rel[tl.b0 + q] = (uint16_t)(tl.bucket >= kBigBucket ? 0 : P.blk_off[tl.b0 + q] - tl.off);
+    if (tl.bucket < kBigBucket && tl.nb < kRelMax) {  // 16-B slot {rel_0..rel_{nb-1}, nnz} streamed with the tile
+      tl.rel_off = (int32_t)pool.size();
+      for (int q = 0; q < tl.nb; ++q) pool.push_back(rel[tl.b0 + q]);
+      pool.push_back((uint16_t)tl.nnz);
+      while (pool.size() % 8) pool.push_back(0);
+    }
+  }
+  pool.resize(pool.size() + 64, 0);
   for (int64_t b = 0; b < nb; ++b) orig[b] = rp[P.perm[b]];
   int64_t *d_perm = nullptr, *d_boff = nullptr;
   if ((s = dev_alloc(p, &d_perm, nb)) || (s = dev_alloc(p, &d_boff, nb))) return fail(s);
   CUDA_TRY(cudaMemsetAsync(p->d_dest, 0, p->a_stride * sizeof(int32_t), p->stream));
   CUDA_TRY(cudaMemsetAsync(p->d_c, 0, p->a_stride * sizeof(float), p->stream));
   CUDA_TRY(cudaMemsetAsync(p->d_a, 0, (size_t)p->a_stride * p->M * sizeof(float), p->stream));
+  if ((s = dev_alloc(p, &p->d_rel_pool, pool.size()))) return fail(s);
+  CUDA_TRY(cudaMemsetAsync(p->d_tiles, 0, (nt + 8) * sizeof(Tile), p->stream));
   CUDA_TRY(cudaMemcpyAsync(p->d_tiles, P.tiles.data(), nt * sizeof(Tile), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(cudaMemcpyAsync(p->d_rel_pool, pool.data(), pool.size() * sizeof(uint16_t), cudaMemcpyHostToDevice,
+                           p->stream));
   CUDA_TRY(cudaMemcpyAsync(p->d_blk_rel, rel.data(), nb * sizeof(uint16_t), cudaMemcpyHostToDevice, p->stream));
   CUDA_TRY(cudaMemcpyAsync(p->d_orig_off, orig.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));
   CUDA_TRY(cudaMemcpyAsync(d_perm, P.perm.data(), nb * sizeof(int64_t), cudaMemcpyHostToDevice, p->stream));

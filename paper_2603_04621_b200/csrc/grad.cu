@@ -67,6 +67,9 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void red_add_f64(double* a, double v) {  // fire-and-forget fp64 reduction
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -157,7 +160,8 @@ __device__ __forceinline__ void solver_update(Solver& S, double r, double u, con
 
 // ---------------------------------------------------------------- shared memory
 struct SmemHead {
-  uint64_t mbar[kWarps][2];
+  uint64_t mbar[kWarps][2];       // data stages (tile arrays + block offsets)
+  uint64_t mbar_desc[kWarps][2];  // descriptor-chunk slots
   double red[2][kWarps][4];
   int32_t slot[16];
 };
@@ -179,7 +183,7 @@ struct Ctx {
   // contribution of one positive x (fp64) to A x, the objective scalars and x_out
   __device__ __forceinline__ void emit(int j, float cval, const float* av, double x, double vs, int b, int e) {
 #pragma unroll
-    for (int f = 0; f < M; ++f) atomicAdd(p.acc + (size_t)f * p.J + j, (double)av[f] * x);
+    for (int f = 0; f < M; ++f) red_add_f64(p.acc + (size_t)f * p.J + j, (double)av[f] * x);
     cx += (double)cval * x;
     reg += 0.5 * gamma * vs * x * x;
     nx += 1.f;
@@ -360,10 +364,220 @@ struct SumsF {
 };
 __device__ __forceinline__ float capsumf(float u, float nC) { return nC > 0.f ? u * nC : 0.f; }
 
+// ---- generic exact solve for one round (out of line: keeps the fast path's registers).
+// Candidates cm (bit k: entry q + k G of the block), frame origin ref (fl32 min of s for
+// the simplex, the K-th smallest s for box-cut).  d = fl32((s - ref)/gamma_i) with s exact,
+// so every entry near a breakpoint is O(max(r, u)) in this frame; a safeguarded Newton in
+// fp32 (Illinois secant / bisection fallback) finds the partition and the threshold is then
+// recomputed in fp64 from it: phi = (r - u|C| + sum_M d)/|M|.
+struct Acc {
+  double cx, reg;
+  float nx;
+};
+
+template <int M, bool LAMS, bool WX, int LG, int E>
+__device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, int start, bool active,
+                                          int b, double vs, double ginv, uint32_t cm, float ref) {
+  C.cx = C.reg = 0.0;
+  C.nx = 0.f;
+  constexpr int G = 1 << LG;
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;
+  const int q = lane & (G - 1);
+  const int kind = p.kind;
+  const double r = p.r, u = p.u;
+  const float rf = p.r, uf = p.u;
+  const double refd = (double)ref;
+  float d[E];
+  float dmax = -kInfF, dmn = kInfF;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    d[k] = kInfF;
+    if (cm >> k & 1u) {
+      d[k] = (float)((score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv);
+      dmax = fmaxf(dmax, d[k]);
+      dmn = fminf(dmn, d[k]);
+    }
+  }
+  dmn = tmin<G>(dmn);
+  const double phi_free64 = -refd * ginv;
+  const float phi_free = (float)fmax(fmin(phi_free64, 1e30), -1e30);
+  auto local = [&](float ph) {
+    SumsF s{0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      if (d[k] < ph) {
+        if (d[k] > ph - uf) {
+          s.nM += 1.f;
+          s.sM += d[k];
+        } else {
+          s.nC += 1.f;
+        }
+      }
+    }
+    s.nM = tsum<G>(s.nM);
+    s.sM = tsum<G>(s.sM);
+    s.nC = tsum<G>(s.nC);
+    return s;
+  };
+  const float hi0 = kind == DL_PROJ_SIMPLEX ? fminf(phi_free, dmn + rf) : fminf(phi_free, tmax<G>(dmax) + uf);
+  SolverF S;
+  S.done = true;
+  S.free = true;
+  S.phi = phi_free;
+  S.lo = S.hi = S.Flo = S.Fhi = 0.f;
+  S.side = 0;
+  SumsF cur = local(hi0);
+  if (active) {
+    const float F = capsumf(uf, cur.nC) + hi0 * cur.nM - cur.sM;
+    S.lo = dmn;  // F(d_min) = 0
+    S.Flo = 0.f;
+    S.hi = hi0;
+    S.Fhi = F;
+    S.phi = hi0;
+    S.free = hi0 == phi_free && F <= rf;
+    S.done = S.free || F == rf;
+  }
+  for (int it = 0; it < 200 && __any_sync(kFull, !S.done); ++it) {
+    if (!S.done) {
+      float cand = cur.nM > 0.f ? (rf - capsumf(uf, cur.nC) + cur.sM) / cur.nM : __int_as_float(0x7fc00000);
+      if (!(cand > S.lo && cand < S.hi)) {
+        cand = S.Fhi > S.Flo ? S.lo + (rf - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5f * (S.lo + S.hi);
+        if (!(cand > S.lo && cand < S.hi)) cand = 0.5f * (S.lo + S.hi);
+      }
+      if (cand == S.phi) S.done = true;
+      else S.phi = cand;
+    }
+    const bool want = !S.done;
+    if (!__any_sync(kFull, want)) break;
+    cur = local(S.phi);
+    if (want) {
+      const float F = capsumf(uf, cur.nC) + S.phi * cur.nM - cur.sM;
+      if (F > rf) {
+        S.hi = S.phi;
+        S.Fhi = F;
+        if (S.side == 1) S.Flo = rf + 0.5f * (S.Flo - rf);
+        S.side = 1;
+      } else if (F < rf) {
+        S.lo = S.phi;
+        S.Flo = F;
+        if (S.side == -1) S.Fhi = rf + 0.5f * (S.Fhi - rf);
+        S.side = -1;
+      } else {
+        S.done = true;
+      }
+      if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
+    }
+  }
+  const float ph32 = S.phi;
+  double sM = 0.0;
+  float nM = 0.f, nC = 0.f;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if (d[k] < ph32) {
+      if (d[k] > ph32 - uf) {
+        nM += 1.f;
+        sM += (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
+      } else {
+        nC += 1.f;
+      }
+    }
+  }
+  nM = tsum<G>(nM);
+  nC = tsum<G>(nC);
+  sM = tsum<G>(sM);
+  if (!active) return Acc{0.0, 0.0, 0.f};
+  const double ph = S.free ? phi_free64 : (nM > 0.f ? (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM : (double)ph32);
+  const float margin = 1e-5f * fmaxf(fabsf(ph32), 1.f);
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if ((cm >> k & 1u) && d[k] < ph32 + margin) {
+      const int e = q + k * G;
+      const double dd = (score_smem(C, sd, sc, sa, cap, start + e) - refd) * ginv;
+      const double x = fmin(fmax(ph - dd, 0.0), u);
+      if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e, x, vs, b, e);
+    }
+  }
+  return Acc{C.cx, C.reg, C.nx};
+}
+
+// ---- box-cut round (out of line): fp32 scan, window above the K-th smallest s
+// (active d < phi <= d_(K) + u, K = ceil(r/u)), then the generic exact solve.
+template <int M, bool LAMS, bool WX, int LG, int E>
+__device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, float slack, int start,
+                                          int len, bool active, int b, double vs, double ginv) {
+  constexpr int G = 1 << LG;
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;
+  const int q = lane & (G - 1);
+  const double r = p.r, u = p.u;
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  const int lim = len - q;
+  float s32[E];
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    const int ee = start + q + k * G;
+    const int j = (int)min((unsigned)sd[ee], Jm1);
+    float sv = sc[ee];
+#pragma unroll
+    for (int f = 0; f < M; ++f) sv = fmaf(sa[f * cap + ee], C.lam(f, j), sv);
+    s32[k] = k * G < lim ? sv : kInfF;
+  }
+  const int K = (int)ceil(r / u);
+  float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
+  uint32_t excl = 0;
+  bool sat = !active;
+  if (K <= 8) {
+    for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
+      float ml = kInfF;
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
+      const float m = tmin<G>(ml);
+      float c = 0.f;
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (!(excl >> k & 1u) && s32[k] == m) {
+          c += 1.f;
+          excl |= 1u << k;
+        }
+      c = tsum<G>(c);
+      if (!sat) {
+        if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
+          sat = true;
+        } else {
+          cnt += c;
+          sk = m;
+          if (cnt >= (float)K) sat = true;
+        }
+      }
+    }
+  }
+  uint32_t cm = 0;
+  if (sat) {
+    const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (s32[k] <= T) cm |= 1u << k;
+  } else {  // K > 8: every entry is a candidate
+#pragma unroll
+    for (int k = 0; k < E; ++k)
+      if (s32[k] < kInfF) cm |= 1u << k;
+  }
+  if (!active) cm = 0;
+  return generic_round<M, LAMS, WX, LG, E>(C, stage, lane, start, active, b, vs, ginv, cm, sat ? sk : 0.f);
+}
+
 // Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
 template <int M, bool LAMS, bool WX, int LG, int E>
-__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane, float slack, int relA,
-                           int relB) {
+__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane, float slack,
+                           const uint16_t* rel_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
   const GradArgs& p = C.p;
@@ -374,26 +588,23 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   const int gi = lane >> LG, q = lane & (G - 1);
   const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
   const int nrounds = (tl.nb + NG - 1) / NG;
-  const double r = p.r, u = p.u;
-  const float rf = p.r, uf = p.u;
   const int kind = p.kind;
   const unsigned Jm1 = (unsigned)p.J - 1u;
   for (int rd = 0; rd < nrounds; ++rd) {
     const int bb = rd * NG + gi;
     const bool active = bb < tl.nb;
     const int b = tl.b0 + bb;
-    // block bounds: relative offsets of the tile's blocks were prefetched into relA (blocks
-    // 0..31) / relB (32..63) of the lanes; tiles with more blocks read them directly
-    int start, end;
-    if (tl.nb < 63) {
-      const int ia = bb, ib = bb + 1;
-      const int sa0 = __shfl_sync(kFull, relA, ia & 31), sb0 = __shfl_sync(kFull, relB, ia & 31);
-      const int sa1 = __shfl_sync(kFull, relA, ib & 31), sb1 = __shfl_sync(kFull, relB, ib & 31);
-      start = ia < 32 ? sa0 : sb0;
-      end = ib < 32 ? sa1 : sb1;
-    } else {
-      start = active ? (int)__ldg(p.blk_rel + b) : 0;
-      end = active ? (bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz) : 0;
+    // block bounds: streamed into shared memory with the tile ({rel_0..rel_{nb-1}, nnz}), or
+    // read from global memory for tiles with many blocks
+    int start = 0, end = 0;
+    if (active) {
+      if (tl.rel_off >= 0) {
+        start = rel_s[bb];
+        end = rel_s[bb + 1];
+      } else {
+        start = (int)__ldg(p.blk_rel + b);
+        end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
+      }
     }
     if (!active) start = end = 0;
     const int len = end - start;
@@ -403,6 +614,13 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         vs = (double)__ldg(p.vsq + b);
         ginv = C.invgamma * (double)__ldg(p.vinv + b);
       }
+    }
+    if (kind == DL_PROJ_BOXCUT) {
+      const Acc a = boxcut_round<M, LAMS, WX, LG, E>(C, stage, lane, slack, start, len, active, b, vs, ginv);
+      C.cx += a.cx;
+      C.reg += a.reg;
+      C.nx += a.nx;
+      continue;
     }
     // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family).
     // Reads past the block end stay inside the stage buffers (tail padding); their dest is
@@ -425,94 +643,59 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     // ---- candidates: entries that can have x > 0.  |fl32(s) - s| <= M 2^-24 B per entry with
     // B the launch-wide magnitude bound; `slack` = 2^-19 (M+1) B covers two such errors 8x over.
     uint32_t cm = 0;
-    float ref = 0.f;
-    if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0
+    if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0: no coupling inside the block, x = clip(-s/gamma_i, 0, u)
 #pragma unroll
       for (int k = 0; k < E; ++k)
         if (s32[k] <= slack) cm |= 1u << k;
-    } else if (kind == DL_PROJ_SIMPLEX) {  // active d < phi <= r  =>  s - s_min < gamma_i r
-      ref = tmin<G>(lmin);
-      const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
-#pragma unroll
-      for (int k = 0; k < E; ++k)
-        if (s32[k] <= T) cm |= 1u << k;
-    } else {  // box-cut: active d < phi <= d_(K) + u, K = ceil(r/u): window above the K-th smallest s
-      const int K = (int)ceil(r / u);
-      float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
-      uint32_t excl = 0;
-      bool sat = !active;
-      if (K <= 8) {
-        for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
-          float ml = kInfF;
-#pragma unroll
-          for (int k = 0; k < E; ++k)
-            if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
-          const float m = tmin<G>(ml);
-          float c = 0.f;
-#pragma unroll
-          for (int k = 0; k < E; ++k)
-            if (!(excl >> k & 1u) && s32[k] == m) {
-              c += 1.f;
-              excl |= 1u << k;
-            }
-          c = tsum<G>(c);
-          if (!sat) {
-            if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
-              sat = true;
-            } else {
-              cnt += c;
-              sk = m;
-              if (cnt >= (float)K) sat = true;
-            }
-          }
-        }
-      }
-      ref = sat ? sk : 0.f;
-      if (sat) {
-        const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-          if (s32[k] <= T) cm |= 1u << k;
-      } else {  // K > 8: every entry is a candidate
-#pragma unroll
-        for (int k = 0; k < E; ++k)
-          if (s32[k] < kInfF) cm |= 1u << k;
-      }
-    }
-    if (!active) cm = 0;
-    if (kind == DL_PROJ_BOX) {  // no coupling inside the block: x = clip(-s/gamma_i, 0, u) per entry
+      if (!active) cm = 0;
       while (cm) {
         const int k = __ffs(cm) - 1;
         cm &= cm - 1;
         const int e = q + k * G, ee = start + e;
-        const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), u);
+        const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), (double)p.u);
         if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ee, x, vs, b, e);
       }
       continue;
     }
-    const double refd = (double)ref;
+    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
+    const float ref = tmin<G>(lmin);
+    const double r = p.r;
+    {
+      const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= T) cm |= 1u << k;
+    }
+    if (!active) cm = 0;
     const int nc = __popc(cm);
-    if (kind == DL_PROJ_SIMPLEX && __all_sync(kFull, nc <= 3)) {
-      // ---- simplex, <= 3 candidates per lane: exact fp64 Michelot on the candidates only
-      double d0 = kInfD, d1 = kInfD, d2 = kInfD;
-      int e0 = -1, e1 = -1, e2 = -1;
-      uint32_t m = cm;
+    if (!__all_sync(kFull, nc <= 3)) {
+      const Acc a = generic_round<M, LAMS, WX, LG, E>(C, stage, lane, start, active, b, vs, ginv, cm, ref);
+      C.cx += a.cx;
+      C.reg += a.reg;
+      C.nx += a.nx;
+      continue;
+    }
+    // ---- simplex, <= 3 candidates per lane: exact fp64 on the candidates only
+    const double refd = (double)ref;
+    const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
+    const int e0 = cm ? q + (__ffs(cm) - 1) * G : -1;
+    const double d0 = e0 >= 0 ? (score_smem(C, sd, sc, sa, cap, start + e0) - refd) * ginv : kInfD;
+    const int n1 = tcount<G>(nc >= 1, gmask), n2 = tcount<G>(nc >= 2, gmask);
+    const int T = n1 + n2 + tcount<G>(nc >= 3, gmask);  // candidates of the group
+    if (__any_sync(kFull, T >= 2)) {
+      // Michelot on the <= 3 candidates per lane
+      int e1 = -1, e2 = -1;
+      double d1 = kInfD, d2 = kInfD;
+      uint32_t m = cm & (cm - 1);
       if (m) {
-        e0 = q + (__ffs(m) - 1) * G;
+        e1 = q + (__ffs(m) - 1) * G;
+        d1 = (score_smem(C, sd, sc, sa, cap, start + e1) - refd) * ginv;
         m &= m - 1;
-        d0 = (score_smem(C, sd, sc, sa, cap, start + e0) - refd) * ginv;
         if (m) {
-          e1 = q + (__ffs(m) - 1) * G;
-          m &= m - 1;
-          d1 = (score_smem(C, sd, sc, sa, cap, start + e1) - refd) * ginv;
-          if (m) {
-            e2 = q + (__ffs(m) - 1) * G;
-            d2 = (score_smem(C, sd, sc, sa, cap, start + e2) - refd) * ginv;
-          }
+          e2 = q + (__ffs(m) - 1) * G;
+          d2 = (score_smem(C, sd, sc, sa, cap, start + e2) - refd) * ginv;
         }
       }
-      const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
-      const int T = tcount<G>(e0 >= 0, gmask) + tcount<G>(e1 >= 0, gmask) + tcount<G>(e2 >= 0, gmask);
       // |d_min| <= slack/gamma_i (ref = fl32 minimum), so F(r + slack/gamma_i) >= r
       double phi = fmin(phi_free, r + (double)slack * ginv);
       bool free = false, done = !active || T <= 1;
@@ -534,166 +717,46 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         }
         first = false;
       }
-      if (active) {
-        if (T == 1) {  // a single candidate: x = clip(-s/gamma_i, 0, r)
-          if (e0 >= 0) {
-            const double x = fmin(fmax(phi_free - d0, 0.0), r);
-            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
-          }
-        } else {
-          const double ph = free ? phi_free : phi;
-          if (e0 >= 0) {
-            const double x = fmax(ph - d0, 0.0);
-            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
-          }
-          if (e1 >= 0) {
-            const double x = fmax(ph - d1, 0.0);
-            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e1, x, vs, b, e1);
-          }
-          if (e2 >= 0) {
-            const double x = fmax(ph - d2, 0.0);
-            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e2, x, vs, b, e2);
-          }
+      if (active && T >= 2) {
+        const double ph = free ? phi_free : phi;
+        if (e0 >= 0) {
+          const double x = fmax(ph - d0, 0.0);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
         }
-      }
-      continue;
-    }
-    // ---- generic path (box-cut, or > 3 candidates in a lane): exact s of the candidates,
-    // d = fl32((s - ref)/gamma_i) with ref = min s (simplex) or the K-th smallest s (box-cut), so
-    // every entry near a breakpoint is O(max(r, u)) in this frame; safeguarded Newton in fp32
-    // finds the partition, the threshold is then recomputed in fp64 from it.
-    float d[E];
-    float dmax = -kInfF, dmn = kInfF;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      d[k] = kInfF;
-      if (cm >> k & 1u) {
-        d[k] = (float)((score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv);
-        dmax = fmaxf(dmax, d[k]);
-        dmn = fminf(dmn, d[k]);
-      }
-    }
-    dmn = tmin<G>(dmn);
-    const double phi_free64 = -refd * ginv;
-    const float phi_free = (float)fmax(fmin(phi_free64, 1e30), -1e30);
-    auto local = [&](float ph) {
-      SumsF s{0.f, 0.f, 0.f};
-#pragma unroll
-      for (int k = 0; k < E; ++k) {
-        if (d[k] < ph) {
-          if (d[k] > ph - uf) {
-            s.nM += 1.f;
-            s.sM += d[k];
-          } else {
-            s.nC += 1.f;
-          }
+        if (e1 >= 0) {
+          const double x = fmax(ph - d1, 0.0);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e1, x, vs, b, e1);
         }
-      }
-      s.nM = tsum<G>(s.nM);
-      s.sM = tsum<G>(s.sM);
-      s.nC = tsum<G>(s.nC);
-      return s;
-    };
-    float hi0 = kind == DL_PROJ_SIMPLEX ? fminf(phi_free, dmn + rf) : fminf(phi_free, tmax<G>(dmax) + uf);
-    SolverF S;
-    S.done = true;
-    S.free = true;
-    S.phi = phi_free;
-    S.lo = S.hi = S.Flo = S.Fhi = 0.f;
-    S.side = 0;
-    SumsF cur = local(hi0);
-    if (active) {
-      const float F = capsumf(uf, cur.nC) + hi0 * cur.nM - cur.sM;
-      S.lo = dmn;  // F(d_min) = 0
-      S.Flo = 0.f;
-      S.hi = hi0;
-      S.Fhi = F;
-      S.phi = hi0;
-      S.free = hi0 == phi_free && F <= rf;
-      S.done = S.free || F == rf;
-    }
-    for (int it = 0; it < 200 && __any_sync(kFull, !S.done); ++it) {
-      if (!S.done) {
-        float cand = cur.nM > 0.f ? (rf - capsumf(uf, cur.nC) + cur.sM) / cur.nM : __int_as_float(0x7fc00000);
-        if (!(cand > S.lo && cand < S.hi)) {
-          cand = S.Fhi > S.Flo ? S.lo + (rf - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5f * (S.lo + S.hi);
-          if (!(cand > S.lo && cand < S.hi)) cand = 0.5f * (S.lo + S.hi);
-        }
-        if (cand == S.phi) S.done = true;
-        else S.phi = cand;
-      }
-      const bool want = !S.done;
-      if (!__any_sync(kFull, want)) break;
-      cur = local(S.phi);
-      if (want) {
-        const float F = capsumf(uf, cur.nC) + S.phi * cur.nM - cur.sM;
-        if (F > rf) {
-          S.hi = S.phi;
-          S.Fhi = F;
-          if (S.side == 1) S.Flo = rf + 0.5f * (S.Flo - rf);
-          S.side = 1;
-        } else if (F < rf) {
-          S.lo = S.phi;
-          S.Flo = F;
-          if (S.side == -1) S.Fhi = rf + 0.5f * (S.Fhi - rf);
-          S.side = -1;
-        } else {
-          S.done = true;
-        }
-        if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
-      }
-    }
-    // exact threshold from the partition at S.phi: phi = (r - u|C| + sum_M d)/|M|
-    const float ph32 = S.phi;
-    double sM = 0.0;
-    float nM = 0.f, nC = 0.f;
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      if (d[k] < ph32) {
-        if (d[k] > ph32 - uf) {
-          nM += 1.f;
-          sM += (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
-        } else {
-          nC += 1.f;
+        if (e2 >= 0) {
+          const double x = fmax(ph - d2, 0.0);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e2, x, vs, b, e2);
         }
       }
     }
-    nM = tsum<G>(nM);
-    nC = tsum<G>(nC);
-    sM = tsum<G>(sM);
-    if (!active) continue;
-    const double ph = S.free ? phi_free64
-                             : (nM > 0.f ? (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM : (double)ph32);
-    const float margin = 1e-5f * fmaxf(fabsf(ph32), 1.f);
-#pragma unroll
-    for (int k = 0; k < E; ++k) {
-      if ((cm >> k & 1u) && d[k] < ph32 + margin) {
-        const int e = q + k * G;
-        const double dd = (score_smem(C, sd, sc, sa, cap, start + e) - refd) * ginv;
-        const double x = fmin(fmax(ph - dd, 0.0), u);
-        if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e, x, vs, b, e);
-      }
+    if (T == 1 && e0 >= 0) {  // a single candidate (the minimum): x = clip(-s/gamma_i, 0, r)
+      const double x0 = phi_free - d0;
+      if (x0 > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x0 < r ? x0 : r, vs, b, e0);
     }
   }
 }
 
 template <int M, bool LAMS, bool WX>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
-                                               float slack, int relA, int relB) {
+                                               float slack, const uint16_t* rel_s) {
   switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, relA, relB); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, relA, relB); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, relA, relB); break;
-    case 6: small_tile<M, LAMS, WX, 3, 8>(C, tl, stage, lane, slack, relA, relB); break;
-    case 7: small_tile<M, LAMS, WX, 4, 8>(C, tl, stage, lane, slack, relA, relB); break;
-    default: small_tile<M, LAMS, WX, 5, 8>(C, tl, stage, lane, slack, relA, relB); break;
+    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, rel_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, rel_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, rel_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, slack, rel_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, slack, rel_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, slack, rel_s); break;
   }
 }
 
 template <int M, bool LAMS, bool WX>
-__global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const GradArgs p) {
+__global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_constant__ GradArgs p) {
   extern __shared__ __align__(128) char smem[];
   SmemHead* head = reinterpret_cast<SmemHead*>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -746,85 +809,103 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const GradArgs 
     }
   }
 
-  // ---- phase 2: small tiles, each warp on its own double-buffered TMA stream.  Tiles are
-  // claimed in chunks of kChunk (one atomic per chunk, claimed a chunk ahead); tile
-  // descriptors are loaded two tiles ahead and block offsets one tile ahead, so neither the
-  // atomic nor the descriptor loads sit on the critical path.
+  // ---- phase 2: small tiles.  Each warp runs its own asynchronous stream: tiles are claimed
+  // in chunks of kChunk (one atomic per chunk, claimed a chunk ahead); the chunk's tile
+  // descriptors arrive by a 128-B bulk copy into a shared slot; every tile's dest / c / a_k
+  // arrays and its block offsets arrive by bulk copies into a double-buffered stage.  No
+  // global load sits on the critical path of a tile.
   {
     constexpr int kChunk = 4;
     const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
     char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
+    char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMetaBytes;
+    const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
+    const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
     uint64_t* bars = head->mbar[warp];
+    uint64_t* dbars = head->mbar_desc[warp];
+    if (lane == 0) {
+      mbar_init(&dbars[0], 1);
+      mbar_init(&dbars[1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
     auto grab = [&]() {
-      int ti = 0;
-      if (lane == 0) ti = atomicAdd(p.ctr + kNumBigPhases, 1) * kChunk + s_begin;
-      return __shfl_sync(kFull, ti, 0);
+      int c = 0;
+      if (lane == 0) c = atomicAdd(p.ctr + kNumBigPhases, 1);
+      return s_begin + kChunk * __shfl_sync(kFull, c, 0);  // first tile of the chunk
     };
-    auto load_desc = [&](int ti) {
-      Tile t{};
-      t.nb = 0;
-      if (ti < s_end) t = p.tiles[ti];
-      return t;
-    };
-    auto load_rel = [&](const Tile& t, int& ra, int& rb) {
-      ra = rb = 0;
-      if (t.nb > 0 && t.nb < 63) {
-        const int i0 = lane, i1 = lane + 32;
-        ra = i0 < t.nb ? (int)__ldg(p.blk_rel + t.b0 + i0) : (i0 == t.nb ? t.nnz : 0);
-        rb = i1 < t.nb ? (int)__ldg(p.blk_rel + t.b0 + i1) : (i1 == t.nb ? t.nnz : 0);
+    auto issue_desc = [&](int first, int slot) {
+      if (lane == 0 && first < s_end) {
+        fence_proxy_async();
+        mbar_expect_tx(&dbars[slot], kChunk * (uint32_t)sizeof(Tile));
+        tma_bulk_g2s(meta + slot * 128, p.tiles + first, kChunk * (uint32_t)sizeof(Tile), &dbars[slot]);
       }
     };
-    auto issue = [&](const Tile& t, int st) {
+    auto issue_tile = [&](const Tile& t, int st) {
       if (lane == 0) {
         const uint32_t n4 = (uint32_t)((t.nnz + kAlign - 1) / kAlign * kAlign);
         const uint32_t bytes = n4 * 4u;
+        const uint32_t rbytes = t.rel_off >= 0 ? (uint32_t)((2 * (t.nb + 1) + 15) & ~15) : 0u;
         char* dst = mybuf + (size_t)st * stage_bytes;
         fence_proxy_async();
-        mbar_expect_tx(&bars[st], bytes * (2u + M));
+        mbar_expect_tx(&bars[st], bytes * (2u + M) + rbytes);
         tma_bulk_g2s(dst, p.dest + t.off, bytes, &bars[st]);
         tma_bulk_g2s(dst + (size_t)p.tile_cap * 4, p.c + t.off, bytes, &bars[st]);
 #pragma unroll
         for (int f = 0; f < M; ++f)
           tma_bulk_g2s(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st]);
+        if (rbytes) tma_bulk_g2s(meta + 256 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
       }
     };
-    int cb = grab(), nbase = grab();  // current / next chunk base
-    int pos = 0;
-    auto ahead = [&](int k) {  // index of the tile k places after the current one
-      const int q2 = pos + k;
-      const int ti = q2 < kChunk ? cb + q2 : nbase + (q2 - kChunk);
-      const int limit = q2 < kChunk ? cb + kChunk : nbase + kChunk;
-      return (ti < s_end && ti < limit) ? ti : s_end;
-    };
-    uint32_t phase[2] = {0u, 0u};
-    int st = 0;
-    int cur = cb < s_end ? cb : s_end;
-    Tile tcur = load_desc(cur);
-    Tile tn1 = load_desc(ahead(1));
-    int relA, relB;
-    load_rel(tcur, relA, relB);
-    if (cur < s_end) issue(tcur, 0);
-    while (cur < s_end) {
-      const int n1 = ahead(1);
-      if (n1 < s_end) issue(tn1, st ^ 1);
-      const Tile tn2 = load_desc(ahead(2));
-      int nA, nB;
-      load_rel(tn1, nA, nB);
+    uint32_t phase[2] = {0u, 0u}, dphase[2] = {0u, 0u};
+    int c0 = grab(), c1 = grab();
+    int ds = 0;  // descriptor slot of chunk c0
+    issue_desc(c0, 0);
+    issue_desc(c1, 1);
+    int c2 = grab();
+    int pos = 0, st = 0;
+    Tile t{};
+    bool have = c0 < s_end;
+    if (have) {
+      mbar_wait(&dbars[0], dphase[0]);
+      dphase[0] ^= 1u;
+      t = dslot[0];
+      issue_tile(t, 0);
+    }
+    while (have) {
+      // descriptor of the next tile: same chunk, or the first of the next chunk
+      Tile tn{};
+      bool nhave;
+      const bool same = pos + 1 < kChunk && c0 + pos + 1 < s_end;
+      if (same) {
+        tn = dslot[ds * kChunk + pos + 1];
+        nhave = true;
+      } else {
+        nhave = c1 < s_end;
+        if (nhave) {
+          mbar_wait(&dbars[ds ^ 1], dphase[ds ^ 1]);
+          dphase[ds ^ 1] ^= 1u;
+          tn = dslot[(ds ^ 1) * kChunk];
+        }
+      }
+      if (nhave) issue_tile(tn, st ^ 1);
       mbar_wait(&bars[st], phase[st]);
       phase[st] ^= 1u;
-      small_dispatch<M, LAMS, WX>(C, tcur, mybuf + (size_t)st * stage_bytes, lane, slack, relA, relB);
+      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, slack, rslot + st * 64);
       __syncwarp();
-      // advance
-      if (++pos == kChunk) {
+      if (same) {
+        ++pos;
+      } else {  // chunk c0 done: its descriptor slot takes chunk c2
+        __syncwarp();
+        issue_desc(c2, ds);
+        c0 = c1;
+        c1 = c2;
+        ds ^= 1;
         pos = 0;
-        cb = nbase;
-        nbase = cb < s_end ? grab() : s_end;
+        c2 = c1 < s_end ? grab() : s_end;
       }
-      cur = n1;
-      tcur = tn1;
-      tn1 = tn2;
-      relA = nA;
-      relB = nB;
+      t = tn;
+      have = nhave;
       st ^= 1;
     }
   }

@@ -22,6 +22,8 @@ constexpr int kAlign = 4;          // entries: 16-byte TMA alignment of every ti
 constexpr int kWarps = 16;         // warps per CTA of the fused kernel
 constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
+constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
+constexpr int kMetaBytes = 512;    // per warp: 2 descriptor-chunk slots (128 B) + 2 rel slots (128 B)
 
 struct alignas(16) Tile {
   int64_t off;     // first entry (multiple of kAlign)
@@ -29,7 +31,8 @@ struct alignas(16) Tile {
   int32_t b0;      // first block (layout order)
   int32_t nb;      // blocks in the tile
   int32_t bucket;  // t = floor(log2 len) + 1 of its blocks
-  int32_t pad0, pad1;
+  int32_t rel_off; // start (uint16 units, multiple of 8) of the tile's block offsets in rel_pool, or -1
+  int32_t pad1;
 };
 static_assert(sizeof(Tile) == 32, "tile descriptor is 32 bytes");
 
@@ -75,6 +78,7 @@ struct GradArgs {
   const Tile* tiles;
   int32_t ph_begin[kNumBigPhases + 2];
   const uint16_t* blk_rel;
+  const uint16_t* rel_pool; // per small tile with < kRelMax blocks: 16-B aligned {rel_0..rel_{nb-1}, nnz}
   const float* vsq;        // per block v_i^2, or nullptr
   const float* vinv;       // per block 1/v_i^2 (with vsq)
   const int64_t* orig_off; // per block original CSR offset (primal output)

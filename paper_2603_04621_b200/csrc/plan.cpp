@@ -40,6 +40,7 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
   auto open_tile = [&](int t) {
     off = (off + kAlign - 1) / kAlign * kAlign;
     Tile tl{};
+    tl.rel_off = -1;
     tl.off = off;
     tl.b0 = (int32_t)b;
     tl.bucket = t;
@@ -85,13 +86,13 @@ static constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per CTA on sm_100
 
 size_t fused_smem_bytes(int32_t m, int32_t J, int32_t tile_cap, int lambda_in_smem) {
   size_t lam = lambda_in_smem ? ((size_t)m * J * 4 + 127) / 128 * 128 : 0;
-  return kSmemFixed + lam + (size_t)kWarps * 2 * tile_cap * (8 + 4 * (size_t)m);
+  return kSmemFixed + lam + (size_t)kWarps * (2 * tile_cap * (8 + 4 * (size_t)m) + kMetaBytes);
 }
 
 int32_t tile_cap_rule(int32_t m, int32_t J, int* lambda_in_smem) {
   auto cap_for = [&](int lam) -> int64_t {
     int64_t lamb = lam ? ((int64_t)m * J * 4 + 127) / 128 * 128 : 0;
-    int64_t budget = (int64_t)kSmemMax - (int64_t)kSmemFixed - lamb;
+    int64_t budget = (int64_t)kSmemMax - (int64_t)kSmemFixed - lamb - (int64_t)kWarps * kMetaBytes;
     int64_t cap = budget / (kWarps * 2 * (8 + 4 * (int64_t)m));
     cap = cap / kAlign * kAlign;
     return std::min<int64_t>(cap, 2048);
