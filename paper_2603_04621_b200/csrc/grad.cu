@@ -34,6 +34,15 @@ namespace dl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCmax = 8;   // candidates per lane on the register fast path
+constexpr int kRcpN = 64;  // 1/n table for the Michelot threshold (sum/n within 1 ulp)
+__constant__ double c_rcp[kRcpN + 1] = {
+    0.0,        1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,  1.0 / 8,  1.0 / 9,  1.0 / 10,
+    1.0 / 11,   1.0 / 12,   1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21,
+    1.0 / 22,   1.0 / 23,   1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32,
+    1.0 / 33,   1.0 / 34,   1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39, 1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43,
+    1.0 / 44,   1.0 / 45,   1.0 / 46, 1.0 / 47, 1.0 / 48, 1.0 / 49, 1.0 / 50, 1.0 / 51, 1.0 / 52, 1.0 / 53, 1.0 / 54,
+    1.0 / 55,   1.0 / 56,   1.0 / 57, 1.0 / 58, 1.0 / 59, 1.0 / 60, 1.0 / 61, 1.0 / 62, 1.0 / 63, 1.0 / 64};
 #define kInfF __int_as_float(0x7f800000)
 #define kInfD __longlong_as_double(0x7ff0000000000000LL)
 
@@ -392,12 +401,15 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
   const float rf = p.r, uf = p.u;
   const double refd = (double)ref;
   float d[E];
+  double d64[E];
   float dmax = -kInfF, dmn = kInfF;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     d[k] = kInfF;
+    d64[k] = kInfD;
     if (cm >> k & 1u) {
-      d[k] = (float)((score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv);
+      d64[k] = (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
+      d[k] = (float)d64[k];
       dmax = fmaxf(dmax, d[k]);
       dmn = fminf(dmn, d[k]);
     }
@@ -472,33 +484,48 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
       if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
     }
   }
+  // exact threshold: Newton in fp64 on the exact partition, started from the fp32 partition
+  // phi = (r - u|C| + sum_M d)/|M| and repeated until the partition is stable
   const float ph32 = S.phi;
-  double sM = 0.0;
-  float nM = 0.f, nC = 0.f;
+  double ph = S.free ? phi_free64 : (double)ph32;
+  bool fin = !active || S.free;
+  bool use32 = true;
+  for (int it = 0; it < 8 && __any_sync(kFull, !fin); ++it) {
+    double sM = 0.0;
+    float nM = 0.f, nC = 0.f;
 #pragma unroll
-  for (int k = 0; k < E; ++k) {
-    if (d[k] < ph32) {
-      if (d[k] > ph32 - uf) {
-        nM += 1.f;
-        sM += (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
+    for (int k = 0; k < E; ++k) {
+      const bool lt = use32 ? d[k] < ph32 : d64[k] < ph;
+      const bool cp = use32 ? d[k] <= ph32 - uf : d64[k] <= ph - u;
+      if (lt) {
+        if (!cp) {
+          nM += 1.f;
+          sM += d64[k];
+        } else {
+          nC += 1.f;
+        }
+      }
+    }
+    nM = tsum<G>(nM);
+    nC = tsum<G>(nC);
+    sM = tsum<G>(sM);
+    use32 = false;
+    if (!fin) {
+      if (nM > 0.f) {
+        const double np = (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM;
+        fin = np == ph;
+        ph = np;
       } else {
-        nC += 1.f;
+        fin = true;  // flat F: any phi of the piece is a root (x is 0 or u there)
       }
     }
   }
-  nM = tsum<G>(nM);
-  nC = tsum<G>(nC);
-  sM = tsum<G>(sM);
   if (!active) return Acc{0.0, 0.0, 0.f};
-  const double ph = S.free ? phi_free64 : (nM > 0.f ? (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM : (double)ph32);
-  const float margin = 1e-5f * fmaxf(fabsf(ph32), 1.f);
 #pragma unroll
   for (int k = 0; k < E; ++k) {
-    if ((cm >> k & 1u) && d[k] < ph32 + margin) {
-      const int e = q + k * G;
-      const double dd = (score_smem(C, sd, sc, sa, cap, start + e) - refd) * ginv;
-      const double x = fmin(fmax(ph - dd, 0.0), u);
-      if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e, x, vs, b, e);
+    if (cm >> k & 1u) {
+      const double x = fmin(fmax(ph - d64[k], 0.0), u);
+      if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + q + k * G, x, vs, b, q + k * G);
     }
   }
   return Acc{C.cx, C.reg, C.nx};
@@ -577,7 +604,7 @@ __device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, 
 // Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
 template <int M, bool LAMS, bool WX, int LG, int E>
 __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane, float slack,
-                           const uint16_t* rel_s) {
+                           const uint16_t* rel_s, uint16_t* cand_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
   const GradArgs& p = C.p;
@@ -667,91 +694,126 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         if (s32[k] <= T) cm |= 1u << k;
     }
     if (!active) cm = 0;
+    // ---- compaction: the group's candidates (entry indices) are packed into a per-warp
+    // shared list so that lane q of the group owns candidates q, q+G, q+2G, q+3G (<= 4 G).
     const int nc = __popc(cm);
-    if (!__all_sync(kFull, nc <= 3)) {
+    int incl = nc;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o, G);
+      if (q >= o) incl += v;
+    }
+    const int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
+    if (!__all_sync(kFull, T <= 4 * G)) {
       const Acc a = generic_round<M, LAMS, WX, LG, E>(C, stage, lane, start, active, b, vs, ginv, cm, ref);
       C.cx += a.cx;
       C.reg += a.reg;
       C.nx += a.nx;
       continue;
     }
-    // ---- simplex, <= 3 candidates per lane: exact fp64 on the candidates only
+    {
+      uint32_t m = cm;
+      int o = gi * 4 * G + incl - nc;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        cand_s[o++] = (uint16_t)(start + q + k * G);
+      }
+    }
+    __syncwarp();
+    const int pmax = (__reduce_max_sync(kFull, (unsigned)T) + G - 1) >> LG;  // warp-uniform
     const double refd = (double)ref;
     const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
-    const int e0 = cm ? q + (__ffs(cm) - 1) * G : -1;
-    const double d0 = e0 >= 0 ? (score_smem(C, sd, sc, sa, cap, start + e0) - refd) * ginv : kInfD;
-    const int n1 = tcount<G>(nc >= 1, gmask), n2 = tcount<G>(nc >= 2, gmask);
-    const int T = n1 + n2 + tcount<G>(nc >= 3, gmask);  // candidates of the group
-    if (__any_sync(kFull, T >= 2)) {
-      // Michelot on the <= 3 candidates per lane
-      int e1 = -1, e2 = -1;
-      double d1 = kInfD, d2 = kInfD;
-      uint32_t m = cm & (cm - 1);
-      if (m) {
-        e1 = q + (__ffs(m) - 1) * G;
-        d1 = (score_smem(C, sd, sc, sa, cap, start + e1) - refd) * ginv;
-        m &= m - 1;
-        if (m) {
-          e2 = q + (__ffs(m) - 1) * G;
-          d2 = (score_smem(C, sd, sc, sa, cap, start + e2) - refd) * ginv;
-        }
-      }
-      // |d_min| <= slack/gamma_i (ref = fl32 minimum), so F(r + slack/gamma_i) >= r
-      double phi = fmin(phi_free, r + (double)slack * ginv);
-      bool free = false, done = !active || T <= 1;
-      int cprev = -1;
-      bool first = true;
-      while (__any_sync(kFull, !done)) {
-        const bool i0 = d0 < phi, i1 = d1 < phi, i2 = d2 < phi;
-        const int cnt = tcount<G>(i0, gmask) + tcount<G>(i1, gmask) + tcount<G>(i2, gmask);
-        const double sm = tsum<G>((i0 ? d0 : 0.0) + (i1 ? d1 : 0.0) + (i2 ? d2 : 0.0));
-        if (!done) {
-          if (first && phi == phi_free && phi * cnt - sm <= r) {
-            free = true;
-            done = true;
-          } else {
-            phi = (r + sm) / cnt;  // Michelot: exact threshold of the current set
-            done = cnt == cprev;   // set unchanged => phi is the root
-            cprev = cnt;
-          }
-        }
-        first = false;
-      }
-      if (active && T >= 2) {
-        const double ph = free ? phi_free : phi;
-        if (e0 >= 0) {
-          const double x = fmax(ph - d0, 0.0);
-          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x, vs, b, e0);
-        }
-        if (e1 >= 0) {
-          const double x = fmax(ph - d1, 0.0);
-          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e1, x, vs, b, e1);
-        }
-        if (e2 >= 0) {
-          const double x = fmax(ph - d2, 0.0);
-          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + e2, x, vs, b, e2);
+    double d64[4];
+    int ei[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      d64[c] = kInfD;
+      ei[c] = -1;
+      if (c < pmax) {
+        const int idx = q + c * G;
+        if (idx < T) {
+          const int ee = cand_s[gi * 4 * G + idx];
+          d64[c] = (score_smem(C, sd, sc, sa, cap, ee) - refd) * ginv;
+          ei[c] = ee;
         }
       }
     }
-    if (T == 1 && e0 >= 0) {  // a single candidate (the minimum): x = clip(-s/gamma_i, 0, r)
-      const double x0 = phi_free - d0;
-      if (x0 > 0.0) emit_smem(C, sd, sc, sa, cap, start + e0, x0 < r ? x0 : r, vs, b, e0);
+    // Michelot in fp64 on the candidates (every candidate has d <= r + 2 slack/gamma_i and
+    // F(r + slack/gamma_i) >= r, so the first set is all of them): phi_{k+1} = (r + sum_{S_k} d)/|S_k|,
+    // S_{k+1} = {d < phi_{k+1}}, until |S| is stable.  1/|S| from a table (within 1 ulp).
+    double phi = 0.0;
+    bool free = false, done = !active || T <= 1;
+    {
+      // free (theta = 0) iff F(phi_free) = sum max(phi_free - d, 0) <= r; if phi_free > r + slack/gamma_i
+      // the minimum alone exceeds r, otherwise every entry with d < phi_free is a candidate.
+      const double rs = r + (double)slack * ginv;
+      double sl = 0.0, fl = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pmax && ei[c] >= 0) {
+          sl += d64[c];
+          fl += fmax(phi_free - d64[c], 0.0);
+        }
+      const double sm = tsum<G>(sl);
+      const double ff = tsum<G>(fl);
+      if (!done) {
+        if (phi_free <= rs && ff <= r) {
+          free = true;
+          done = true;
+        } else {
+          phi = (r + sm) * (T <= kRcpN ? c_rcp[T] : 1.0 / T);  // Michelot from all candidates
+        }
+      }
     }
+    int cprev = T;
+    for (int it = 0; it < 32 && __any_sync(kFull, !done); ++it) {
+      int cl = 0;
+      double sl = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pmax && d64[c] < phi) {
+          cl += 1;
+          sl += d64[c];
+        }
+      const int cnt = tsum<G>(cl);
+      const double sm = tsum<G>(sl);
+      if (!done) {
+        if (cnt == cprev || cnt == 0) {
+          done = true;
+        } else {
+          cprev = cnt;
+          phi = (r + sm) * (cnt <= kRcpN ? c_rcp[cnt] : 1.0 / cnt);
+        }
+      }
+    }
+    if (active) {
+      const double ph = (free || T == 1) ? phi_free : phi;
+      const double cap_x = T == 1 ? r : kInfD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < pmax && ei[c] >= 0) {
+          const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ei[c], x, vs, b, ei[c] - start);
+        }
+      }
+    }
+    __syncwarp();  // the candidate list is rewritten by the next round
   }
 }
 
 template <int M, bool LAMS, bool WX>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
-                                               float slack, const uint16_t* rel_s) {
+                                               float slack, const uint16_t* rel_s, uint16_t* cand_s) {
   switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, rel_s); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, rel_s); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, rel_s); break;
-    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, slack, rel_s); break;
-    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, slack, rel_s); break;
-    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, slack, rel_s); break;
+    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
   }
 }
 
@@ -821,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMetaBytes;
     const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
     const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // [128] candidate list
     uint64_t* bars = head->mbar[warp];
     uint64_t* dbars = head->mbar_desc[warp];
     if (lane == 0) {
@@ -829,11 +892,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
+    // lane 0 claims a chunk; the value is broadcast only when it is used (a chunk later), so
+    // the atomic's latency is not waited on
     auto grab = [&]() {
       int c = 0;
       if (lane == 0) c = atomicAdd(p.ctr + kNumBigPhases, 1);
-      return s_begin + kChunk * __shfl_sync(kFull, c, 0);  // first tile of the chunk
+      return c;
     };
+    auto first_of = [&](int raw) { return s_begin + kChunk * __shfl_sync(kFull, raw, 0); };
     auto issue_desc = [&](int first, int slot) {
       if (lane == 0 && first < s_end) {
         fence_proxy_async();
@@ -858,11 +924,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       }
     };
     uint32_t phase[2] = {0u, 0u}, dphase[2] = {0u, 0u};
-    int c0 = grab(), c1 = grab();
+    int c0 = first_of(grab()), c1 = first_of(grab());
     int ds = 0;  // descriptor slot of chunk c0
     issue_desc(c0, 0);
     issue_desc(c1, 1);
-    int c2 = grab();
+    int c2raw = grab();
     int pos = 0, st = 0;
     Tile t{};
     bool have = c0 < s_end;
@@ -891,18 +957,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (nhave) issue_tile(tn, st ^ 1);
       mbar_wait(&bars[st], phase[st]);
       phase[st] ^= 1u;
-      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, slack, rslot + st * 64);
+      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, slack, rslot + st * 64, cslot);
       __syncwarp();
       if (same) {
         ++pos;
       } else {  // chunk c0 done: its descriptor slot takes chunk c2
+        const int c2 = first_of(c2raw);
         __syncwarp();
         issue_desc(c2, ds);
         c0 = c1;
         c1 = c2;
         ds ^= 1;
         pos = 0;
-        c2 = c1 < s_end ? grab() : s_end;
+        c2raw = c1 < s_end ? grab() : (s_end - s_begin) / kChunk + 1;  // past the end
       }
       t = tn;
       have = nhave;

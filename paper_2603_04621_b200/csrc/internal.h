@@ -23,7 +23,7 @@ constexpr int kWarps = 16;         // warps per CTA of the fused kernel
 constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
 constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
-constexpr int kMetaBytes = 512;    // per warp: 2 descriptor-chunk slots (128 B) + 2 rel slots (128 B)
+constexpr int kMetaBytes = 768;    // per warp: 2 descriptor-chunk slots (128 B) + 2 rel slots (128 B) + candidate list (256 B)
 
 struct alignas(16) Tile {
   int64_t off;     // first entry (multiple of kAlign)
