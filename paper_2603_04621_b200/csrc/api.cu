@@ -63,7 +63,7 @@ struct dl_problem {
   bool own_stream = false;
   int64_t I = 0, nnz = 0;
   int32_t J = 0, M = 1, kind = 0;
-  float r = 1.f, u = INFINITY;
+  double r = 1.0, u = INFINITY;
   // layout
   Plan plan;
   int32_t tile_cap = 256, lam_smem = 0, num_sms = 148, ctas = 148;
@@ -293,8 +293,8 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
   p->J = d->num_dests;
   p->M = d->num_families;
   p->kind = d->proj_kind;
-  p->r = d->proj_kind == DL_PROJ_BOX ? INFINITY : (float)d->proj_r;
-  p->u = d->proj_kind == DL_PROJ_SIMPLEX ? INFINITY : (float)d->proj_u;
+  p->r = d->proj_kind == DL_PROJ_BOX ? INFINITY : d->proj_r;
+  p->u = d->proj_kind == DL_PROJ_SIMPLEX ? INFINITY : d->proj_u;
   auto fail = [&](dl_status s) {
     free_all(p);
     delete p;

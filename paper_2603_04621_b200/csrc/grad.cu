@@ -486,9 +486,17 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
   }
   // exact threshold: Newton in fp64 on the exact partition, started from the fp32 partition
   // phi = (r - u|C| + sum_M d)/|M| and repeated until the partition is stable
+  // theta = 0 decided exactly: F(phi_free) = sum clip(phi_free - d, 0, u) <= r in fp64
+  double ff = 0.0;
+#pragma unroll
+  for (int k = 0; k < E; ++k)
+    if (cm >> k & 1u) ff += fmin(fmax(phi_free64 - d64[k], 0.0), u);
+  ff = tsum<G>(ff);
+  const bool free64 = phi_free64 <= 1e30 && ff <= r;
+  if (S.free && !free64) S.phi = phi_free;  // the fp32 test was too optimistic: Newton from phi_free
   const float ph32 = S.phi;
-  double ph = S.free ? phi_free64 : (double)ph32;
-  bool fin = !active || S.free;
+  double ph = free64 ? phi_free64 : (double)ph32;
+  bool fin = !active || free64;
   bool use32 = true;
   for (int it = 0; it < 8 && __any_sync(kFull, !fin); ++it) {
     double sM = 0.0;

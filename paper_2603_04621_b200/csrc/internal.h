@@ -87,7 +87,7 @@ struct GradArgs {
   const double* gamma_ptr; // device gamma (solver) or nullptr -> gamma_val
   double gamma_val;
   const float* slack;      // device: 2^-19 (m+1) (max|c| + sum_f max|a_f| max|lambda_f|)
-  float r, u;
+  double r, u;             // polytope caps (inf where absent)
   int32_t kind;
   int32_t tile_cap;
   int32_t lam_smem;
