@@ -252,7 +252,8 @@ def main():
 
     # ---- end to end through the host-buffer entry (pinned host lambda in, gradient + objective out)
     n = gp.n
-    lam_h = torch.from_numpy(np.full(n, 1e-3, np.float32)).pin_memory()
+    _, l2_now = gp.dual()  # the dual point the timed steps were at
+    lam_h = torch.from_numpy(l2_now.astype(np.float32)).pin_memory()
     grad_h = torch.zeros(n, dtype=torch.float64).pin_memory()
     obj_h = torch.zeros(4, dtype=torch.float64).pin_memory()
     grad_d, obj_d = gp.new_grad_buffers()
@@ -284,7 +285,7 @@ def main():
     # ---- time to a 1e-3 relative dual gap (continuation 0.16 -> 0.01, Jacobi; R11)
     gap = None
     if not args.no_gap:
-        ref_iters = 4000
+        ref_iters = 8000
         gp.agd_init(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3, init_step=1e-5,
                     history_cap=ref_iters)
         gp.solve(ref_iters)

@@ -17,7 +17,7 @@
 //   bucket t), <= 8 entries per lane.
 //   Fast filter: s is first formed in fp32 (one FMA per family) and only entries with
 //   s32 - min s32 <= gamma_i r + slack can have x > 0 on the simplex (active d < phi <= r),
-//   resp. s32 < slack on the box.  Those candidates alone are re-formed exactly in fp64
+//   resp. s32 < slack on the box (slack: the block's fp32 rounding bound).  Those candidates alone are re-formed exactly in fp64
 //   (products of fp32 are exact in fp64) and the threshold is solved in fp64 (Michelot,
 //   one or two candidates per lane: shuffle reductions over the group).  Box-cut blocks
 //   and groups with more candidates take the generic exact path: fp64 d for every entry,
@@ -542,7 +542,7 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
 // ---- box-cut round (out of line): fp32 scan, window above the K-th smallest s
 // (active d < phi <= d_(K) + u, K = ceil(r/u)), then the generic exact solve.
 template <int M, bool LAMS, bool WX, int LG, int E>
-__device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, float slack, int start,
+__device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, int start,
                                           int len, bool active, int b, double vs, double ginv) {
   constexpr int G = 1 << LG;
   const GradArgs& p = C.p;
@@ -555,15 +555,23 @@ __device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, 
   const unsigned Jm1 = (unsigned)p.J - 1u;
   const int lim = len - q;
   float s32[E];
+  float lmag = 0.f;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     const int ee = start + q + k * G;
     const int j = (int)min((unsigned)sd[ee], Jm1);
-    float sv = sc[ee];
+    const float cv = sc[ee];
+    float sv = cv, mg = fabsf(cv);
 #pragma unroll
-    for (int f = 0; f < M; ++f) sv = fmaf(sa[f * cap + ee], C.lam(f, j), sv);
+    for (int f = 0; f < M; ++f) {
+      const float av = sa[f * cap + ee], lv = C.lam(f, j);
+      sv = fmaf(av, lv, sv);
+      mg = fmaf(fabsf(av), fabsf(lv), mg);
+    }
     s32[k] = k * G < lim ? sv : kInfF;
+    if (k * G < lim) lmag = fmaxf(lmag, mg);
   }
+  const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
   const int K = (int)ceil(r / u);
   float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
   uint32_t excl = 0;
@@ -611,7 +619,7 @@ __device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, 
 
 // Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
 template <int M, bool LAMS, bool WX, int LG, int E>
-__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane, float slack,
+__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
                            const uint16_t* rel_s, uint16_t* cand_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
@@ -651,7 +659,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       }
     }
     if (kind == DL_PROJ_BOXCUT) {
-      const Acc a = boxcut_round<M, LAMS, WX, LG, E>(C, stage, lane, slack, start, len, active, b, vs, ginv);
+      const Acc a = boxcut_round<M, LAMS, WX, LG, E>(C, stage, lane, start, len, active, b, vs, ginv);
       C.cx += a.cx;
       C.reg += a.reg;
       C.nx += a.nx;
@@ -665,20 +673,29 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     const float* sap = sa + start + q;
     const int lim = len - q;  // slot k of this lane is inside the block iff k*G < lim
     float s32[E];
-    float lmin = kInfF;
+    float lmin = kInfF, lmag = 0.f;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       const int j = (int)min((unsigned)sdp[k * G], Jm1);
-      float sv = scp[k * G];
+      const float cv = scp[k * G];
+      float sv = cv, mg = fabsf(cv);
 #pragma unroll
-      for (int f = 0; f < M; ++f) sv = fmaf(sap[f * cap + k * G], C.lam(f, j), sv);
-      s32[k] = k * G < lim ? sv : kInfF;
+      for (int f = 0; f < M; ++f) {
+        const float av = sap[f * cap + k * G], lv = C.lam(f, j);
+        sv = fmaf(av, lv, sv);
+        mg = fmaf(fabsf(av), fabsf(lv), mg);
+      }
+      const bool in = k * G < lim;
+      s32[k] = in ? sv : kInfF;
       lmin = fminf(lmin, s32[k]);
+      if (in) lmag = fmaxf(lmag, mg);
     }
-    // ---- candidates: entries that can have x > 0.  |fl32(s) - s| <= M 2^-24 B per entry with
-    // B the launch-wide magnitude bound; `slack` = 2^-19 (M+1) B covers two such errors 8x over.
+    // ---- candidates: entries that can have x > 0.  With one rounding per FMA,
+    // |fl32(s) - s| <= M 2^-24 (|c| + sum_f |a_f lambda_f|) = M 2^-24 mag per entry; the block
+    // slack 2^-22 (M+1) max(mag) covers the two errors of s_j - s_min with a 2x margin.
     uint32_t cm = 0;
     if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0: no coupling inside the block, x = clip(-s/gamma_i, 0, u)
+      const float slack = 2.3841858e-7f * (M + 1) * lmag;  // 2^-22 (M+1) mag (lane bound suffices)
 #pragma unroll
       for (int k = 0; k < E; ++k)
         if (s32[k] <= slack) cm |= 1u << k;
@@ -694,6 +711,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     }
     // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
     const float ref = tmin<G>(lmin);
+    const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);  // 2^-22 (M+1) max mag of the block
     const double r = p.r;
     {
       const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
@@ -812,16 +830,16 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
 
 template <int M, bool LAMS, bool WX>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
-                                               float slack, const uint16_t* rel_s, uint16_t* cand_s) {
+                                               const uint16_t* rel_s, uint16_t* cand_s) {
   switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, slack, rel_s, cand_s); break;
-    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
-    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
-    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, slack, rel_s, cand_s); break;
+    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, rel_s, cand_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, rel_s, cand_s); break;
   }
 }
 
@@ -849,7 +867,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   __syncthreads();
 
   const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
-  const float slack = *p.slack;  // fl32 error bound of s (see small_tile), per launch
   Ctx<M, LAMS, WX> C(p, lam_s, gamma);
 
   // ---- phase 1: big blocks, groups of 16 / 8 / 4 / 2 warps; barrier ids unique per group
@@ -965,7 +982,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (nhave) issue_tile(tn, st ^ 1);
       mbar_wait(&bars[st], phase[st]);
       phase[st] ^= 1u;
-      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, slack, rslot + st * 64, cslot);
+      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot);
       __syncwarp();
       if (same) {
         ++pos;
