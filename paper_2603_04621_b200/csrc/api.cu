@@ -76,6 +76,8 @@ struct dl_problem {
   uint16_t* d_rel_pool = nullptr;
   int64_t* d_orig_off = nullptr;
   double* d_gscratch = nullptr;
+  DeferEntry* d_defer = nullptr;
+  int32_t defer_cap = 0;
   int64_t gscratch_per_cta = 0;
   float cmax = 0.f, amax[4] = {0.f, 0.f, 0.f, 0.f};
   float* d_slack = nullptr;  // [2]: 0 standalone path, 1 solver path
@@ -195,6 +197,8 @@ GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   a.ctr = p->d_ctr;
   a.x_out = x_out;
   a.gscratch = p->d_gscratch;
+  a.defer = p->d_defer;
+  a.defer_cap = p->defer_cap;
   a.gscratch_per_cta = p->gscratch_per_cta;
   return a;
 }
@@ -358,6 +362,10 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
       (s = dev_alloc(p, &p->d_obj_out, 4)) || (s = dev_alloc(p, &p->d_slack, 2)))
     return fail(s);
   if (d->v && ((s = dev_alloc(p, &p->d_vsq, nb)) || (s = dev_alloc(p, &p->d_vinv, nb)))) return fail(s);
+  if (p->kind != DL_PROJ_BOXCUT) {  // queue for simplex blocks deferred by the fused kernel
+    p->defer_cap = (int32_t)std::max<int64_t>(nb, 1);
+    if ((s = dev_alloc(p, &p->d_defer, p->defer_cap))) return fail(s);
+  }
   // global d-scratch for blocks longer than a 16-warp group's shared scratch
   const int64_t smem_scr = (int64_t)kWarps * 2 * p->tile_cap * (8 + 4 * p->M) / 8;  // fp64 d
   if (P.max_len > smem_scr) {

@@ -373,43 +373,31 @@ struct SumsF {
 };
 __device__ __forceinline__ float capsumf(float u, float nC) { return nC > 0.f ? u * nC : 0.f; }
 
-// ---- generic exact solve for one round (out of line: keeps the fast path's registers).
-// Candidates cm (bit k: entry q + k G of the block), frame origin ref (fl32 min of s for
-// the simplex, the K-th smallest s for box-cut).  d = fl32((s - ref)/gamma_i) with s exact,
-// so every entry near a breakpoint is O(max(r, u)) in this frame; a safeguarded Newton in
-// fp32 (Illinois secant / bisection fallback) finds the partition and the threshold is then
-// recomputed in fp64 from it: phi = (r - u|C| + sum_M d)/|M|.
-struct Acc {
-  double cx, reg;
-  float nx;
-};
-
+// ---- generic exact solve for one round (box-cut, or a group with > 4 G simplex candidates).
+// Candidates cm (bit k: entry q + k G of the block), frame origin ref (fl32 min of s for the
+// simplex, the K-th smallest s for box-cut).  d = fl32((s - ref)/gamma_i) with s exact, so every
+// entry near a breakpoint is O(max(r, u)) in this frame; a safeguarded Newton in fp32 (Illinois
+// secant / bisection fallback) finds the partition, then Newton steps in fp64 on the exact
+// partition (exact d recomputed from shared memory) give phi = (r - u|C| + sum_M d)/|M|.
 template <int M, bool LAMS, bool WX, int LG, int E>
-__device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, int start, bool active,
-                                          int b, double vs, double ginv, uint32_t cm, float ref) {
-  C.cx = C.reg = 0.0;
-  C.nx = 0.f;
+__device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+                                              const float* sa, int cap, int q, int start, bool active, int b,
+                                              double vs, double ginv, uint32_t cm, float ref, float (&d)[E]) {
   constexpr int G = 1 << LG;
   const GradArgs& p = C.p;
-  const int cap = p.tile_cap;
-  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
-  const float* sc = reinterpret_cast<const float*>(stage) + cap;
-  const float* sa = sc + cap;
-  const int q = lane & (G - 1);
   const int kind = p.kind;
   const double r = p.r, u = p.u;
   const float rf = p.r, uf = p.u;
   const double refd = (double)ref;
-  float d[E];
-  double d64[E];
+  auto dexact = [&](int k) { return (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv; };
+  // d in fp32 from the caller's fp32 scores (in place): only the partition search uses it; the
+  // fp64 Newton steps below re-derive exact d from shared memory and settle any boundary entry
+  const float ginvf = (float)ginv;
   float dmax = -kInfF, dmn = kInfF;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
-    d[k] = kInfF;
-    d64[k] = kInfD;
+    d[k] = (cm >> k & 1u) ? (d[k] - ref) * ginvf : kInfF;
     if (cm >> k & 1u) {
-      d64[k] = (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv;
-      d[k] = (float)d64[k];
       dmax = fmaxf(dmax, d[k]);
       dmn = fminf(dmn, d[k]);
     }
@@ -484,13 +472,11 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
       if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
     }
   }
-  // exact threshold: Newton in fp64 on the exact partition, started from the fp32 partition
-  // phi = (r - u|C| + sum_M d)/|M| and repeated until the partition is stable
   // theta = 0 decided exactly: F(phi_free) = sum clip(phi_free - d, 0, u) <= r in fp64
   double ff = 0.0;
 #pragma unroll
   for (int k = 0; k < E; ++k)
-    if (cm >> k & 1u) ff += fmin(fmax(phi_free64 - d64[k], 0.0), u);
+    if (cm >> k & 1u) ff += fmin(fmax(phi_free64 - dexact(k), 0.0), u);
   ff = tsum<G>(ff);
   const bool free64 = phi_free64 <= 1e30 && ff <= r;
   if (S.free && !free64) S.phi = phi_free;  // the fp32 test was too optimistic: Newton from phi_free
@@ -503,14 +489,17 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
     float nM = 0.f, nC = 0.f;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
-      const bool lt = use32 ? d[k] < ph32 : d64[k] < ph;
-      const bool cp = use32 ? d[k] <= ph32 - uf : d64[k] <= ph - u;
-      if (lt) {
-        if (!cp) {
-          nM += 1.f;
-          sM += d64[k];
-        } else {
-          nC += 1.f;
+      if (cm >> k & 1u) {
+        const double dd = use32 ? 0.0 : dexact(k);
+        const bool lt = use32 ? d[k] < ph32 : dd < ph;
+        const bool cp = use32 ? d[k] <= ph32 - uf : dd <= ph - u;
+        if (lt) {
+          if (!cp) {
+            nM += 1.f;
+            sM += use32 ? dexact(k) : dd;
+          } else {
+            nC += 1.f;
+          }
         }
       }
     }
@@ -528,97 +517,20 @@ __device__ __noinline__ Acc generic_round(Ctx<M, LAMS, WX> C, const char* stage,
       }
     }
   }
-  if (!active) return Acc{0.0, 0.0, 0.f};
+  if (!active) return;
 #pragma unroll
   for (int k = 0; k < E; ++k) {
     if (cm >> k & 1u) {
-      const double x = fmin(fmax(ph - d64[k], 0.0), u);
+      const double x = fmin(fmax(ph - dexact(k), 0.0), u);
       if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + q + k * G, x, vs, b, q + k * G);
     }
   }
-  return Acc{C.cx, C.reg, C.nx};
-}
-
-// ---- box-cut round (out of line): fp32 scan, window above the K-th smallest s
-// (active d < phi <= d_(K) + u, K = ceil(r/u)), then the generic exact solve.
-template <int M, bool LAMS, bool WX, int LG, int E>
-__device__ __noinline__ Acc boxcut_round(Ctx<M, LAMS, WX> C, const char* stage, int lane, int start,
-                                          int len, bool active, int b, double vs, double ginv) {
-  constexpr int G = 1 << LG;
-  const GradArgs& p = C.p;
-  const int cap = p.tile_cap;
-  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
-  const float* sc = reinterpret_cast<const float*>(stage) + cap;
-  const float* sa = sc + cap;
-  const int q = lane & (G - 1);
-  const double r = p.r, u = p.u;
-  const unsigned Jm1 = (unsigned)p.J - 1u;
-  const int lim = len - q;
-  float s32[E];
-  float lmag = 0.f;
-#pragma unroll
-  for (int k = 0; k < E; ++k) {
-    const int ee = start + q + k * G;
-    const int j = (int)min((unsigned)sd[ee], Jm1);
-    const float cv = sc[ee];
-    float sv = cv, mg = fabsf(cv);
-#pragma unroll
-    for (int f = 0; f < M; ++f) {
-      const float av = sa[f * cap + ee], lv = C.lam(f, j);
-      sv = fmaf(av, lv, sv);
-      mg = fmaf(fabsf(av), fabsf(lv), mg);
-    }
-    s32[k] = k * G < lim ? sv : kInfF;
-    if (k * G < lim) lmag = fmaxf(lmag, mg);
-  }
-  const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
-  const int K = (int)ceil(r / u);
-  float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
-  uint32_t excl = 0;
-  bool sat = !active;
-  if (K <= 8) {
-    for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
-      float ml = kInfF;
-#pragma unroll
-      for (int k = 0; k < E; ++k)
-        if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
-      const float m = tmin<G>(ml);
-      float c = 0.f;
-#pragma unroll
-      for (int k = 0; k < E; ++k)
-        if (!(excl >> k & 1u) && s32[k] == m) {
-          c += 1.f;
-          excl |= 1u << k;
-        }
-      c = tsum<G>(c);
-      if (!sat) {
-        if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
-          sat = true;
-        } else {
-          cnt += c;
-          sk = m;
-          if (cnt >= (float)K) sat = true;
-        }
-      }
-    }
-  }
-  uint32_t cm = 0;
-  if (sat) {
-    const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
-#pragma unroll
-    for (int k = 0; k < E; ++k)
-      if (s32[k] <= T) cm |= 1u << k;
-  } else {  // K > 8: every entry is a candidate
-#pragma unroll
-    for (int k = 0; k < E; ++k)
-      if (s32[k] < kInfF) cm |= 1u << k;
-  }
-  if (!active) cm = 0;
-  return generic_round<M, LAMS, WX, LG, E>(C, stage, lane, start, active, b, vs, ginv, cm, sat ? sk : 0.f);
 }
 
 // Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
-template <int M, bool LAMS, bool WX, int LG, int E>
+// GEN: the kernel variant that solves box-cut and overflowing simplex groups inline (generic
+// path); otherwise overflowing simplex groups are deferred to deferred_kernel.
+template <int M, bool LAMS, bool WX, int LG, int E, bool GEN>
 __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
                            const uint16_t* rel_s, uint16_t* cand_s) {
   constexpr int G = 1 << LG;
@@ -629,7 +541,6 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   const float* sc = reinterpret_cast<const float*>(stage) + cap;
   const float* sa = sc + cap;  // family f at sa + f*cap
   const int gi = lane >> LG, q = lane & (G - 1);
-  const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
   const int nrounds = (tl.nb + NG - 1) / NG;
   const int kind = p.kind;
   const unsigned Jm1 = (unsigned)p.J - 1u;
@@ -649,7 +560,6 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
       }
     }
-    if (!active) start = end = 0;
     const int len = end - start;
     double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
     if (p.vsq) {
@@ -658,16 +568,10 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         ginv = C.invgamma * (double)__ldg(p.vinv + b);
       }
     }
-    if (kind == DL_PROJ_BOXCUT) {
-      const Acc a = boxcut_round<M, LAMS, WX, LG, E>(C, stage, lane, start, len, active, b, vs, ginv);
-      C.cx += a.cx;
-      C.reg += a.reg;
-      C.nx += a.nx;
-      continue;
-    }
-    // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family).
-    // Reads past the block end stay inside the stage buffers (tail padding); their dest is
-    // clamped to [0, J) and their s32 replaced by +inf.
+    // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family)
+    // and the magnitude |c| + sum_f |a_f lambda_f| bounding its rounding error.  Reads past the
+    // block end stay inside the stage buffers (tail padding); their dest is clamped to [0, J)
+    // and their s32 replaced by +inf.
     const int32_t* sdp = sd + start + q;
     const float* scp = sc + start + q;
     const float* sap = sa + start + q;
@@ -709,10 +613,59 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       }
       continue;
     }
-    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
-    const float ref = tmin<G>(lmin);
     const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);  // 2^-22 (M+1) max mag of the block
     const double r = p.r;
+    if (GEN && kind == DL_PROJ_BOXCUT) {
+      // window above the K-th smallest s: active d < phi <= d_(K) + u, K = ceil(r/u)
+      const double u = p.u;
+      const int K = (int)ceil(r / u);
+      float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
+      uint32_t excl = 0;
+      bool sat = !active;
+      if (K <= 8) {
+        for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
+          float ml = kInfF;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
+          const float m = tmin<G>(ml);
+          float c = 0.f;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u) && s32[k] == m) {
+              c += 1.f;
+              excl |= 1u << k;
+            }
+          c = tsum<G>(c);
+          if (!sat) {
+            if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
+              sat = true;
+            } else {
+              cnt += c;
+              sk = m;
+              if (cnt >= (float)K) sat = true;
+            }
+          }
+        }
+      }
+      if (sat) {
+        const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] <= T) cm |= 1u << k;
+      } else {  // K > 8: every entry is a candidate
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] < kInfF) cm |= 1u << k;
+      }
+      if (!active) cm = 0;
+      if constexpr (GEN)
+        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, sat ? sk : 0.f,
+                                          s32);
+      continue;
+    }
+    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
+    const float ref = tmin<G>(lmin);
     {
       const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
 #pragma unroll
@@ -729,13 +682,20 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       const int v = __shfl_up_sync(kFull, incl, o, G);
       if (q >= o) incl += v;
     }
-    const int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
-    if (!__all_sync(kFull, T <= 4 * G)) {
-      const Acc a = generic_round<M, LAMS, WX, LG, E>(C, stage, lane, start, active, b, vs, ginv, cm, ref);
-      C.cx += a.cx;
-      C.reg += a.reg;
-      C.nx += a.nx;
-      continue;
+    int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
+    if constexpr (GEN) {
+      if (!__all_sync(kFull, T <= 4 * G)) {
+        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
+        continue;
+      }
+    } else if (T > 4 * G) {  // defer this block to deferred_kernel (exact generic solve there)
+      if (q == 0) {
+        const int slot = atomicAdd(p.ctr + 6, 1);
+        if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, len};
+      }
+      cm = 0;
+      incl = 0;
+      T = 0;
     }
     {
       uint32_t m = cm;
@@ -828,22 +788,22 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   }
 }
 
-template <int M, bool LAMS, bool WX>
+template <int M, bool LAMS, bool WX, bool GEN>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
                                                const uint16_t* rel_s, uint16_t* cand_s) {
   switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 6: small_tile<M, LAMS, WX, 2, 16>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 7: small_tile<M, LAMS, WX, 3, 16>(C, tl, stage, lane, rel_s, cand_s); break;
-    default: small_tile<M, LAMS, WX, 4, 16>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 3: small_tile<M, LAMS, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
   }
 }
 
-template <int M, bool LAMS, bool WX>
+template <int M, bool LAMS, bool WX, bool GEN>
 __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_constant__ GradArgs p) {
   extern __shared__ __align__(128) char smem[];
   SmemHead* head = reinterpret_cast<SmemHead*>(smem);
@@ -948,7 +908,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
         if (rbytes) tma_bulk_g2s(meta + 256 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
       }
     };
-    uint32_t phase[2] = {0u, 0u}, dphase[2] = {0u, 0u};
+    uint32_t phase = 0u, dphase = 0u;  // mbarrier parities, bit s for slot s (kept in registers)
     int c0 = first_of(grab()), c1 = first_of(grab());
     int ds = 0;  // descriptor slot of chunk c0
     issue_desc(c0, 0);
@@ -958,8 +918,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     Tile t{};
     bool have = c0 < s_end;
     if (have) {
-      mbar_wait(&dbars[0], dphase[0]);
-      dphase[0] ^= 1u;
+      mbar_wait(&dbars[0], dphase & 1u);
+      dphase ^= 1u;
       t = dslot[0];
       issue_tile(t, 0);
     }
@@ -974,15 +934,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       } else {
         nhave = c1 < s_end;
         if (nhave) {
-          mbar_wait(&dbars[ds ^ 1], dphase[ds ^ 1]);
-          dphase[ds ^ 1] ^= 1u;
+          mbar_wait(&dbars[ds ^ 1], (dphase >> (ds ^ 1)) & 1u);
+          dphase ^= 1u << (ds ^ 1);
           tn = dslot[(ds ^ 1) * kChunk];
         }
       }
       if (nhave) issue_tile(tn, st ^ 1);
-      mbar_wait(&bars[st], phase[st]);
-      phase[st] ^= 1u;
-      small_dispatch<M, LAMS, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot);
+      mbar_wait(&bars[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+      small_dispatch<M, LAMS, WX, GEN>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot);
       __syncwarp();
       if (same) {
         ++pos;
@@ -1018,20 +978,109 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   }
 }
 
-template <int M, bool LAMS, bool WX>
+// Deferred simplex blocks (groups whose candidates overflowed the register fast path): one
+// warp per block, staged from global memory into shared memory, generic exact solve.
+template <int M, bool WX>
+__global__ void __launch_bounds__(256) deferred_kernel(const __grid_constant__ GradArgs p) {
+  constexpr int kW = 8;
+  constexpr int kStage = 256;  // entries (blocks here are < 256 long)
+  extern __shared__ __align__(128) char dsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* stage = dsm + (size_t)warp * kStage * (8 + 4 * M);
+  int32_t* sd = reinterpret_cast<int32_t*>(stage);
+  float* sc = reinterpret_cast<float*>(stage) + kStage;
+  float* sa = sc + kStage;
+  const int n = min(p.ctr[6], p.defer_cap);
+  const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
+  GradArgs pl = p;
+  pl.tile_cap = kStage;
+  Ctx<M, false, WX> C(pl, nullptr, gamma);
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  for (int i = blockIdx.x * kW + warp; i < n; i += gridDim.x * kW) {
+    const DeferEntry de = p.defer[i];
+    for (int e = lane; e < kStage; e += 32) {
+      const bool v = e < de.len;
+      sd[e] = v ? __ldg(p.dest + de.off + e) : 0;
+      sc[e] = v ? __ldg(p.c + de.off + e) : 0.f;
+#pragma unroll
+      for (int f = 0; f < M; ++f) sa[f * kStage + e] = v ? __ldg(p.a + f * p.a_stride + de.off + e) : 0.f;
+    }
+    __syncwarp();
+    double vs = 1.0, ginv = C.invgamma;
+    if (p.vsq) {
+      vs = (double)__ldg(p.vsq + de.b);
+      ginv = C.invgamma * (double)__ldg(p.vinv + de.b);
+    }
+    float s32[8];
+    float lmin = kInfF, lmag = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = lane + 32 * k;
+      const int j = (int)min((unsigned)sd[e], Jm1);
+      float sv = sc[e], mg = fabsf(sc[e]);
+#pragma unroll
+      for (int f = 0; f < M; ++f) {
+        const float av = sa[f * kStage + e], lv = C.lam(f, j);
+        sv = fmaf(av, lv, sv);
+        mg = fmaf(fabsf(av), fabsf(lv), mg);
+      }
+      s32[k] = e < de.len ? sv : kInfF;
+      lmin = fminf(lmin, s32[k]);
+      if (e < de.len) lmag = fmaxf(lmag, mg);
+    }
+    const float ref = tmin<32>(lmin);
+    const float slack = 2.3841858e-7f * (M + 1) * tmax<32>(lmag);
+    const float T = ref + ((float)(p.r * gamma * vs) * 1.000001f + slack);
+    uint32_t cm = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (s32[k] <= T) cm |= 1u << k;
+    // the block's entries sit at [0, len) of the warp's stage; orig_off / x_out use de.b
+    generic_round<M, false, WX, 5, 8>(C, sd, sc, sa, kStage, lane, 0, true, de.b, vs, ginv, cm, ref, s32);
+    __syncwarp();
+  }
+  double cx = C.cx, rg = C.reg;
+  float nx = C.nx;
+  for (int o = 16; o > 0; o >>= 1) {
+    cx += __shfl_xor_sync(kFull, cx, o);
+    rg += __shfl_xor_sync(kFull, rg, o);
+    nx += __shfl_xor_sync(kFull, nx, o);
+  }
+  if (lane == 0 && nx > 0.f) {
+    const size_t nn = (size_t)M * p.J;
+    atomicAdd(p.acc + nn + 0, cx);
+    atomicAdd(p.acc + nn + 1, rg);
+    atomicAdd(p.acc + nn + 2, (double)nx);
+  }
+}
+
+template <int M, bool LAMS, bool WX, bool GEN>
 cudaError_t launch_t(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  auto k = fused_grad_kernel<M, LAMS, WX>;
+  auto k = fused_grad_kernel<M, LAMS, WX, GEN>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<ctas, kThreads, smem, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || GEN || !a.defer) return e;
+  const size_t dsmem = (size_t)8 * 256 * (8 + 4 * M);
+  auto dk = deferred_kernel<M, WX>;
+  e = cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+  if (e != cudaSuccess) return e;
+  dk<<<ctas, 256, dsmem, s>>>(a);
   return cudaGetLastError();
 }
 
 template <int M>
 cudaError_t launch_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
   const bool wx = a.x_out != nullptr;
-  if (a.lam_smem) return wx ? launch_t<M, true, true>(a, ctas, smem, s) : launch_t<M, true, false>(a, ctas, smem, s);
-  return wx ? launch_t<M, false, true>(a, ctas, smem, s) : launch_t<M, false, false>(a, ctas, smem, s);
+  if (a.kind == DL_PROJ_BOXCUT) {
+    if (a.lam_smem)
+      return wx ? launch_t<M, true, true, true>(a, ctas, smem, s) : launch_t<M, true, false, true>(a, ctas, smem, s);
+    return wx ? launch_t<M, false, true, true>(a, ctas, smem, s) : launch_t<M, false, false, true>(a, ctas, smem, s);
+  }
+  if (a.lam_smem)
+    return wx ? launch_t<M, true, true, false>(a, ctas, smem, s) : launch_t<M, true, false, false>(a, ctas, smem, s);
+  return wx ? launch_t<M, false, true, false>(a, ctas, smem, s) : launch_t<M, false, false, false>(a, ctas, smem, s);
 }
 
 }  // namespace

@@ -70,6 +70,12 @@ struct AgdDev {
 };
 
 // ---- kernel launch interfaces (implemented in grad.cu / step.cu) ----------
+struct DeferEntry {  // a short simplex block handed from the fused kernel to deferred_kernel
+  int64_t off;       // first entry in the permuted arrays
+  int32_t b;         // block (layout order)
+  int32_t len;
+};
+
 struct GradArgs {
   const int32_t* dest;
   const float* c;
@@ -92,7 +98,9 @@ struct GradArgs {
   int32_t tile_cap;
   int32_t lam_smem;
   double* acc;             // [m*J + 4]
-  int32_t* ctr;            // [8] work-queue counters (zeroed before launch)
+  int32_t* ctr;            // [8] work-queue counters (zeroed before launch); [6] = deferred blocks
+  DeferEntry* defer;       // deferred-block queue (simplex / box kinds)
+  int32_t defer_cap;
   float* x_out;            // primal output (original order) or nullptr
   double* gscratch;        // global fp64 d-scratch for blocks beyond the smem scratch
   int64_t gscratch_per_cta;
