@@ -541,6 +541,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   const float* sc = reinterpret_cast<const float*>(stage) + cap;
   const float* sa = sc + cap;  // family f at sa + f*cap
   const int gi = lane >> LG, q = lane & (G - 1);
+  const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
   const int nrounds = (tl.nb + NG - 1) / NG;
   const int kind = p.kind;
   const unsigned Jm1 = (unsigned)p.J - 1u;
@@ -725,44 +726,32 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         }
       }
     }
-    // Michelot in fp64 on the candidates (every candidate has d <= r + 2 slack/gamma_i and
-    // F(r + slack/gamma_i) >= r, so the first set is all of them): phi_{k+1} = (r + sum_{S_k} d)/|S_k|,
-    // S_{k+1} = {d < phi_{k+1}}, until |S| is stable.  1/|S| from a table (within 1 ulp).
+    // Michelot in fp64 on the candidates for the root phi* of F(phi) = sum max(phi - d, 0) = r
+    // (every active entry is a candidate and phi* <= r + slack/gamma_i, so F over the candidates
+    // is F over the block there): start from all T candidates, phi = (r + sum_S d)/|S|,
+    // S = {d < phi}, until |S| is stable (1/|S| from a table, within 1 ulp).  The threshold is
+    // min(phi_free, phi*): theta = 0 exactly when phi_free <= phi* (F(phi_free) <= r).
     double phi = 0.0;
-    bool free = false, done = !active || T <= 1;
+    bool done = !active || T <= 1;
     {
-      // free (theta = 0) iff F(phi_free) = sum max(phi_free - d, 0) <= r; if phi_free > r + slack/gamma_i
-      // the minimum alone exceeds r, otherwise every entry with d < phi_free is a candidate.
-      const double rs = r + (double)slack * ginv;
-      double sl = 0.0, fl = 0.0;
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        if (c < pmax && ei[c] >= 0) {
-          sl += d64[c];
-          fl += fmax(phi_free - d64[c], 0.0);
-        }
-      const double sm = tsum<G>(sl);
-      const double ff = tsum<G>(fl);
-      if (!done) {
-        if (phi_free <= rs && ff <= r) {
-          free = true;
-          done = true;
-        } else {
-          phi = (r + sm) * (T <= kRcpN ? c_rcp[T] : 1.0 / T);  // Michelot from all candidates
-        }
-      }
-    }
-    int cprev = T;
-    for (int it = 0; it < 32 && __any_sync(kFull, !done); ++it) {
-      int cl = 0;
       double sl = 0.0;
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        if (c < pmax && d64[c] < phi) {
-          cl += 1;
-          sl += d64[c];
+        if (c < pmax && ei[c] >= 0) sl += d64[c];
+      const double sm = tsum<G>(sl);
+      if (!done) phi = (r + sm) * (T <= kRcpN ? c_rcp[T] : 1.0 / T);
+    }
+    int cprev = T;
+    for (int it = 0; it < 32 && __any_sync(kFull, !done); ++it) {
+      int cnt = 0;
+      double sl = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pmax) {
+          const bool in = d64[c] < phi;
+          cnt += tcount<G>(in, gmask);
+          if (in) sl += d64[c];
         }
-      const int cnt = tsum<G>(cl);
       const double sm = tsum<G>(sl);
       if (!done) {
         if (cnt == cprev || cnt == 0) {
@@ -774,7 +763,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       }
     }
     if (active) {
-      const double ph = (free || T == 1) ? phi_free : phi;
+      const double ph = T == 1 ? phi_free : fmin(phi_free, phi);
       const double cap_x = T == 1 ? r : kInfD;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
