@@ -8,13 +8,15 @@ import os
 import shutil
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libdualip.so")
-SOURCES = ["plan.cpp", "grad.cu", "step.cu", "api.cu"]
+SOURCES = ["grad_m1.cu", "grad_m2.cu", "grad_m3.cu", "grad_m4.cu", "plan.cpp", "grad.cu", "step.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -25,34 +27,33 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def build(verbose: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
+def build(verbose: bool = False, extra: list[str] | None = None, out: str = LIB) -> str:
+    """Compile every source (in parallel: the per-m kernel TUs dominate) and link ``out``."""
+    os.makedirs(os.path.dirname(out), exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), *ARCH]
     if verbose:
         common += ["-Xptxas", "-v"]
     common += extra or []
-    for src in SOURCES:
-        obj = os.path.join(LIBDIR, src.rsplit(".", 1)[0] + ".o")
-        cmd = [nvcc(), *common, "-c", os.path.join(CSRC, src), "-o", obj]
-        if src.endswith(".cpp"):
-            cmd = [nvcc(), "-x", "cu", *common, "-c", os.path.join(CSRC, src), "-o", obj]
+    with tempfile.TemporaryDirectory(prefix="dualip_build_") as tmpdir:
+        def compile_one(src):
+            obj = os.path.join(tmpdir, src.rsplit(".", 1)[0] + ".o")
+            lang = ["-x", "cu"] if src.endswith(".cpp") else []
+            r = subprocess.run([nvcc(), *lang, *common, "-c", os.path.join(CSRC, src), "-o", obj],
+                               capture_output=True, text=True)
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+            if verbose and r.stderr:
+                sys.stderr.write(f"---- {src}\n{r.stderr}")
+            return obj
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+            objs = list(ex.map(compile_one, SOURCES))
+        tmp = out + ".tmp"
+        cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-Xlinker", "--no-undefined"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
-        if verbose and r.stderr:
-            sys.stderr.write(r.stderr)
-        objs.append(obj)
-    tmp = LIB + ".tmp"
-    cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-Xlinker", "--no-undefined"]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    for o in objs:
-        os.remove(o)
-    return LIB
-
+            raise RuntimeError(f"link failed:\n{r.stderr}")
+        os.replace(tmp, out)
+    return out
 
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv))

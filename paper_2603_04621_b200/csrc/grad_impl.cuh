@@ -1,0 +1,1084 @@
+// Fused dual-gradient pass (K1).  Included once per family count M by
+// grad_m1.cu .. grad_m4.cu (DL_GRAD_M); launch_fused_grad (grad.cu) dispatches on m.
+//
+// One persistent CTA per SM (16 warps).  For every source block i:
+//   s_ij = c_ij + sum_k a_kij lambda_kj                 (reduced cost)
+//   y_ij = -s_ij / gamma_i,  gamma_i = gamma v_i^2
+//   x_i  = Pi_{C_i}(y_i) = clip(phi - d_ij, 0, u),  d_ij = (s_ij - min_j s_ij)/gamma_i,
+//          phi the threshold of the block polytope (R1, R7)
+//   acc[k*J + j] += a_kij x_ij   (fp64 red.global, only where x_ij > 0)
+//   acc[mJ+0] += c_ij x_ij, acc[mJ+1] += gamma_i/2 x_ij^2, acc[mJ+2] += [x_ij > 0]
+//
+// Work = the tile list of the layout (plan.cpp).
+//  Phase 1 (blocks >= 256 entries, buckets >= 9): multi-warp groups (16/8/4/2 warps for
+//   buckets >=12/11/10/9) read the block from global memory; d in an fp64 scratch.
+//  Phase 2 (short blocks): every warp pulls tiles independently; a tile's dest / c / a_k
+//   arrays arrive by cp.async.bulk (TMA bulk copy) into a per-warp double buffer with an
+//   mbarrier.  A tile's blocks are worked by groups of G = 1..32 lanes (G = 2^(t-3) for
+//   bucket t), <= 8 entries per lane.
+//   Fast filter: s is first formed in fp32 (one FMA per family) and only entries with
+//   s32 - min s32 <= gamma_i r + slack can have x > 0 on the simplex (active d < phi <= r),
+//   resp. s32 < slack on the box (slack: the block's fp32 rounding bound).  Those candidates alone are re-formed exactly in fp64
+//   (products of fp32 are exact in fp64) and the threshold is solved in fp64 (Michelot,
+//   one or two candidates per lane: shuffle reductions over the group).  Box-cut blocks
+//   and groups with more candidates take the generic exact path: fp64 d for every entry,
+//   safeguarded Newton on the piecewise-linear F(phi) = sum clip(phi - d, 0, u) with an
+//   Illinois-secant / bisection fallback.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+#include <cstdint>
+
+#include "internal.h"
+
+namespace dl {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCmax = 8;   // candidates per lane on the register fast path
+constexpr int kRcpN = 64;  // 1/n table for the Michelot threshold (sum/n within 1 ulp)
+__constant__ double c_rcp[kRcpN + 1] = {
+    0.0,        1.0,        1.0 / 2,  1.0 / 3,  1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,  1.0 / 8,  1.0 / 9,  1.0 / 10,
+    1.0 / 11,   1.0 / 12,   1.0 / 13, 1.0 / 14, 1.0 / 15, 1.0 / 16, 1.0 / 17, 1.0 / 18, 1.0 / 19, 1.0 / 20, 1.0 / 21,
+    1.0 / 22,   1.0 / 23,   1.0 / 24, 1.0 / 25, 1.0 / 26, 1.0 / 27, 1.0 / 28, 1.0 / 29, 1.0 / 30, 1.0 / 31, 1.0 / 32,
+    1.0 / 33,   1.0 / 34,   1.0 / 35, 1.0 / 36, 1.0 / 37, 1.0 / 38, 1.0 / 39, 1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43,
+    1.0 / 44,   1.0 / 45,   1.0 / 46, 1.0 / 47, 1.0 / 48, 1.0 / 49, 1.0 / 50, 1.0 / 51, 1.0 / 52, 1.0 / 53, 1.0 / 54,
+    1.0 / 55,   1.0 / 56,   1.0 / 57, 1.0 / 58, 1.0 / 59, 1.0 / 60, 1.0 / 61, 1.0 / 62, 1.0 / 63, 1.0 / 64};
+#define kInfF __int_as_float(0x7f800000)
+#define kInfD __longlong_as_double(0x7ff0000000000000LL)
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void red_add_f64(double* a, double v) {  // fire-and-forget fp64 reduction
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- group reductions
+// Butterflies over aligned groups of G lanes (G a power of two <= 32): every lane of
+// a group ends with bitwise the same value (a+b == b+a in IEEE arithmetic).
+template <class T>
+__device__ __forceinline__ T gsum(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T gmin(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T gmax(T v, int G) {
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------- exact threshold solver
+// F(phi) = u nC + phi nM - sM with M = {phi-u < d < phi}, C = {d <= phi-u} (fp64).
+struct Sums {
+  double nM, sM, nC;
+};
+__device__ __forceinline__ double capsum(double u, double nC) { return nC > 0.0 ? u * nC : 0.0; }
+__device__ __forceinline__ double Fval(double phi, double u, const Sums& s) {
+  return capsum(u, s.nC) + phi * s.nM - s.sM;
+}
+
+struct Solver {
+  double lo, hi, Flo, Fhi, phi;
+  int side;   // last bracket end replaced: +1 hi, -1 lo (Illinois)
+  bool done;
+  bool free;  // theta = 0: the clamp alone is feasible, phi = phi_free
+};
+
+// Start at hi0 (F(hi0) >= r unless hi0 == phi_free); bracket [0, hi0] (F(0) = 0 <= r as d >= 0).
+__device__ __forceinline__ void solver_start(Solver& S, double r, double u, double phi_free, const Sums& s0,
+                                             double hi0) {
+  const double F = Fval(hi0, u, s0);
+  S.lo = 0.0;
+  S.Flo = 0.0;
+  S.hi = hi0;
+  S.Fhi = F;
+  S.phi = hi0;
+  S.side = 0;
+  S.done = false;
+  S.free = false;
+  if (hi0 == phi_free && F <= r) {
+    S.phi = phi_free;
+    S.done = true;
+    S.free = true;
+  } else if (F == r) {
+    S.done = true;
+  }
+}
+// Newton step from the partition at S.phi; falls back to Illinois secant / bisection.
+__device__ __forceinline__ double solver_candidate(Solver& S, double r, double u, const Sums& s) {
+  double cand = s.nM > 0.0 ? (r - capsum(u, s.nC) + s.sM) / s.nM : __longlong_as_double(0x7ff8000000000000LL);
+  if (!(cand > S.lo && cand < S.hi)) {
+    cand = S.Fhi > S.Flo ? S.lo + (r - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5 * (S.lo + S.hi);
+    if (!(cand > S.lo && cand < S.hi)) cand = 0.5 * (S.lo + S.hi);
+  }
+  if (cand == S.phi) S.done = true;
+  return cand;
+}
+__device__ __forceinline__ void solver_update(Solver& S, double r, double u, const Sums& s) {
+  const double F = Fval(S.phi, u, s);
+  if (F > r) {
+    S.hi = S.phi;
+    S.Fhi = F;
+    if (S.side == 1) S.Flo = r + 0.5 * (S.Flo - r);  // Illinois: lo retained twice
+    S.side = 1;
+  } else if (F < r) {
+    S.lo = S.phi;
+    S.Flo = F;
+    if (S.side == -1) S.Fhi = r + 0.5 * (S.Fhi - r);
+    S.side = -1;
+  } else {
+    S.done = true;
+  }
+  if (!(S.hi - S.lo > 4e-16 * fabs(S.hi))) S.done = true;
+}
+
+// ---------------------------------------------------------------- shared memory
+struct SmemHead {
+  uint64_t mbar[kWarps][2];       // data stages (tile arrays + block offsets)
+  uint64_t mbar_desc[kWarps][2];  // descriptor-chunk slots
+  double red[2][kWarps][4];
+  int32_t slot[16];
+};
+static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
+
+template <int M, bool LAMS, bool WX>
+struct Ctx {
+  const GradArgs& p;
+  const float* lam_s;  // shared lambda (LAMS)
+  double gamma, invgamma;
+  double cx = 0.0, reg = 0.0;
+  float nx = 0.f;
+  __device__ Ctx(const GradArgs& pp, const float* ls, double g) : p(pp), lam_s(ls), gamma(g), invgamma(1.0 / g) {}
+
+  __device__ __forceinline__ float lam(int f, int j) const {
+    if constexpr (LAMS) return lam_s[f * p.J + j];
+    return __ldg(p.lam + (size_t)f * p.J + j);
+  }
+  // contribution of one positive x (fp64) to A x, the objective scalars and x_out
+  __device__ __forceinline__ void emit(int j, float cval, const float* av, double x, double vs, int b, int e) {
+#pragma unroll
+    for (int f = 0; f < M; ++f) red_add_f64(p.acc + (size_t)f * p.J + j, (double)av[f] * x);
+    cx += (double)cval * x;
+    reg += 0.5 * gamma * vs * x * x;
+    nx += 1.f;
+    if constexpr (WX) p.x_out[__ldg(p.orig_off + b) + e] = (float)x;
+  }
+};
+
+// ---------------------------------------------------------------- phase 1: big blocks
+struct BigGroup {
+  int gw, G, gtid, warp0, bar, lane, warp;
+  int rb = 0;
+  SmemHead* head;
+  __device__ __forceinline__ void sync() { named_bar(bar, G); }
+  // reduce up to 3 doubles with op (0 sum, 1 min, 2 max); deterministic order
+  template <int N>
+  __device__ __forceinline__ void reduce(double (&v)[N], int op) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      for (int o = 16; o > 0; o >>= 1) {
+        double w = __shfl_xor_sync(kFull, v[i], o);
+        v[i] = op == 0 ? v[i] + w : (op == 1 ? fmin(v[i], w) : fmax(v[i], w));
+      }
+    }
+    const int b = rb;
+    rb ^= 1;
+    if (lane == 0)
+#pragma unroll
+      for (int i = 0; i < N; ++i) head->red[b][warp][i] = v[i];
+    sync();
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double t = head->red[b][warp0][i];
+      for (int w = 1; w < gw; ++w) {
+        const double q = head->red[b][warp0 + w][i];
+        t = op == 0 ? t + q : (op == 1 ? fmin(t, q) : fmax(t, q));
+      }
+      v[i] = t;
+    }
+  }
+};
+
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ double score_global(const Ctx<M, LAMS, WX>& C, int64_t e) {
+  const GradArgs& p = C.p;
+  const int j = __ldg(p.dest + e);
+  double s = (double)__ldg(p.c + e);
+#pragma unroll
+  for (int f = 0; f < M; ++f) s = fma((double)__ldg(p.a + f * p.a_stride + e), (double)C.lam(f, j), s);
+  return s;
+}
+
+template <int M, bool LAMS, bool WX>
+__device__ void big_block(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, double* scr) {
+  const GradArgs& p = C.p;
+  const int len = tl.nnz;
+  const int64_t off = tl.off;
+  const int b = tl.b0;
+  const double r = p.r, u = p.u;
+  // pass 1: exact minimum reduced cost
+  double mn[1] = {DBL_MAX};
+#pragma unroll 4
+  for (int e = g.gtid; e < len; e += g.G) mn[0] = fmin(mn[0], score_global(C, off + e));
+  g.reduce(mn, 1);
+  const double smin = mn[0];
+  const double vs = p.vsq ? (double)__ldg(p.vsq + b) : 1.0;
+  const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + b) : C.invgamma;
+  const double phi_free = -smin * ginv;
+  // pass 2: d = (s - smin)/gamma_i into the scratch (own entries only)
+  double mx[1] = {-DBL_MAX};
+#pragma unroll 4
+  for (int e = g.gtid; e < len; e += g.G) {
+    const double d = (score_global(C, off + e) - smin) * ginv;
+    scr[e] = d;
+    mx[0] = fmax(mx[0], d);
+  }
+  double phi = phi_free;
+  bool free = true;
+  if (p.kind != DL_PROJ_BOX) {
+    if (p.kind == DL_PROJ_BOXCUT) g.reduce(mx, 2);
+    auto eval = [&](double ph) {
+      double v[3] = {0.0, 0.0, 0.0};
+      for (int e = g.gtid; e < len; e += g.G) {
+        const double d = scr[e];
+        if (d < ph) {
+          if (d > ph - u) {
+            v[0] += 1.0;
+            v[1] += d;
+          } else {
+            v[2] += 1.0;
+          }
+        }
+      }
+      g.reduce(v, 0);
+      return Sums{v[0], v[1], v[2]};
+    };
+    const double hi0 = p.kind == DL_PROJ_SIMPLEX ? fmin(phi_free, r) : fmin(phi_free, mx[0] + u);
+    Solver S;
+    Sums cur = eval(hi0);
+    solver_start(S, r, u, phi_free, cur, hi0);
+    for (int it = 0; it < 200 && !S.done; ++it) {
+      const double cand = solver_candidate(S, r, u, cur);
+      if (S.done) break;
+      S.phi = cand;
+      cur = eval(S.phi);
+      solver_update(S, r, u, cur);
+    }
+    phi = S.phi;
+    free = S.free;
+  }
+  for (int e = g.gtid; e < len; e += g.G) {
+    const double d = scr[e];
+    const double x = free ? fmin(fmax(phi_free - d, 0.0), u) : fmin(fmax(phi - d, 0.0), u);
+    if (x > 0.0) {
+      const int j = __ldg(p.dest + off + e);
+      float av[M];
+#pragma unroll
+      for (int f = 0; f < M; ++f) av[f] = __ldg(p.a + f * p.a_stride + off + e);
+      C.emit(j, __ldg(p.c + off + e), av, x, vs, b, e);
+    }
+  }
+  g.sync();  // scratch reuse by the next block of this group
+}
+
+// ---------------------------------------------------------------- phase 2: small tiles
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ double score_smem(const Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+                                             const float* sa, int cap, int ee) {
+  const int j = sd[ee];
+  double s = (double)sc[ee];
+#pragma unroll
+  for (int f = 0; f < M; ++f) s = fma((double)sa[f * cap + ee], (double)C.lam(f, j), s);
+  return s;
+}
+
+template <int M, bool LAMS, bool WX>
+__device__ __forceinline__ void emit_smem(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc, const float* sa,
+                                          int cap, int ee, double x, double vs, int b, int e) {
+  float av[M];
+#pragma unroll
+  for (int f = 0; f < M; ++f) av[f] = sa[f * cap + ee];
+  C.emit(sd[ee], sc[ee], av, x, vs, b, e);
+}
+
+// Compile-time group reductions (G lanes, aligned groups inside the warp).
+template <int G, class T>
+__device__ __forceinline__ T tsum(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+template <int G, class T>
+__device__ __forceinline__ T tmin(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v = min(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+template <int G, class T>
+__device__ __forceinline__ T tmax(T v) {
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) v = max(v, __shfl_xor_sync(kFull, v, o));
+  return v;
+}
+// number of set predicates over the group's lanes (one vote)
+template <int G>
+__device__ __forceinline__ int tcount(bool pred, uint32_t gmask) {
+  return __popc(__ballot_sync(kFull, pred) & gmask);
+}
+
+// fp32 threshold solver state for the generic small path (partition only; the final
+// threshold is recomputed in fp64 from the partition).
+struct SolverF {
+  float lo, hi, Flo, Fhi, phi;
+  int side;
+  bool done, free;
+};
+struct SumsF {
+  float nM, sM, nC;
+};
+__device__ __forceinline__ float capsumf(float u, float nC) { return nC > 0.f ? u * nC : 0.f; }
+
+// ---- generic exact solve for one round (box-cut, or a group with > 4 G simplex candidates).
+// Candidates cm (bit k: entry q + k G of the block), frame origin ref (fl32 min of s for the
+// simplex, the K-th smallest s for box-cut).  d = fl32((s - ref)/gamma_i) with s exact, so every
+// entry near a breakpoint is O(max(r, u)) in this frame; a safeguarded Newton in fp32 (Illinois
+// secant / bisection fallback) finds the partition, then Newton steps in fp64 on the exact
+// partition (exact d recomputed from shared memory) give phi = (r - u|C| + sum_M d)/|M|.
+template <int M, bool LAMS, bool WX, int LG, int E>
+__device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+                                              const float* sa, int cap, int q, int start, bool active, int b,
+                                              double vs, double ginv, uint32_t cm, float ref, float (&d)[E]) {
+  constexpr int G = 1 << LG;
+  const GradArgs& p = C.p;
+  const int kind = p.kind;
+  const double r = p.r, u = p.u;
+  const float rf = p.r, uf = p.u;
+  const double refd = (double)ref;
+  auto dexact = [&](int k) { return (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv; };
+  // d in fp32 from the caller's fp32 scores (in place): only the partition search uses it; the
+  // fp64 Newton steps below re-derive exact d from shared memory and settle any boundary entry
+  const float ginvf = (float)ginv;
+  float dmax = -kInfF, dmn = kInfF;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    d[k] = (cm >> k & 1u) ? (d[k] - ref) * ginvf : kInfF;
+    if (cm >> k & 1u) {
+      dmax = fmaxf(dmax, d[k]);
+      dmn = fminf(dmn, d[k]);
+    }
+  }
+  dmn = tmin<G>(dmn);
+  const double phi_free64 = -refd * ginv;
+  const float phi_free = (float)fmax(fmin(phi_free64, 1e30), -1e30);
+  auto local = [&](float ph) {
+    SumsF s{0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      if (d[k] < ph) {
+        if (d[k] > ph - uf) {
+          s.nM += 1.f;
+          s.sM += d[k];
+        } else {
+          s.nC += 1.f;
+        }
+      }
+    }
+    s.nM = tsum<G>(s.nM);
+    s.sM = tsum<G>(s.sM);
+    s.nC = tsum<G>(s.nC);
+    return s;
+  };
+  const float hi0 = kind == DL_PROJ_SIMPLEX ? fminf(phi_free, dmn + rf) : fminf(phi_free, tmax<G>(dmax) + uf);
+  SolverF S;
+  S.done = true;
+  S.free = true;
+  S.phi = phi_free;
+  S.lo = S.hi = S.Flo = S.Fhi = 0.f;
+  S.side = 0;
+  SumsF cur = local(hi0);
+  if (active) {
+    const float F = capsumf(uf, cur.nC) + hi0 * cur.nM - cur.sM;
+    S.lo = dmn;  // F(d_min) = 0
+    S.Flo = 0.f;
+    S.hi = hi0;
+    S.Fhi = F;
+    S.phi = hi0;
+    S.free = hi0 == phi_free && F <= rf;
+    S.done = S.free || F == rf;
+  }
+  for (int it = 0; it < 200 && __any_sync(kFull, !S.done); ++it) {
+    if (!S.done) {
+      float cand = cur.nM > 0.f ? (rf - capsumf(uf, cur.nC) + cur.sM) / cur.nM : __int_as_float(0x7fc00000);
+      if (!(cand > S.lo && cand < S.hi)) {
+        cand = S.Fhi > S.Flo ? S.lo + (rf - S.Flo) * (S.hi - S.lo) / (S.Fhi - S.Flo) : 0.5f * (S.lo + S.hi);
+        if (!(cand > S.lo && cand < S.hi)) cand = 0.5f * (S.lo + S.hi);
+      }
+      if (cand == S.phi) S.done = true;
+      else S.phi = cand;
+    }
+    const bool want = !S.done;
+    if (!__any_sync(kFull, want)) break;
+    cur = local(S.phi);
+    if (want) {
+      const float F = capsumf(uf, cur.nC) + S.phi * cur.nM - cur.sM;
+      if (F > rf) {
+        S.hi = S.phi;
+        S.Fhi = F;
+        if (S.side == 1) S.Flo = rf + 0.5f * (S.Flo - rf);
+        S.side = 1;
+      } else if (F < rf) {
+        S.lo = S.phi;
+        S.Flo = F;
+        if (S.side == -1) S.Fhi = rf + 0.5f * (S.Fhi - rf);
+        S.side = -1;
+      } else {
+        S.done = true;
+      }
+      if (!(S.hi - S.lo > 2.4e-7f * fabsf(S.hi))) S.done = true;
+    }
+  }
+  // theta = 0 decided exactly: F(phi_free) = sum clip(phi_free - d, 0, u) <= r in fp64
+  double ff = 0.0;
+#pragma unroll
+  for (int k = 0; k < E; ++k)
+    if (cm >> k & 1u) ff += fmin(fmax(phi_free64 - dexact(k), 0.0), u);
+  ff = tsum<G>(ff);
+  const bool free64 = phi_free64 <= 1e30 && ff <= r;
+  if (S.free && !free64) S.phi = phi_free;  // the fp32 test was too optimistic: Newton from phi_free
+  const float ph32 = S.phi;
+  double ph = free64 ? phi_free64 : (double)ph32;
+  bool fin = !active || free64;
+  bool use32 = true;
+  for (int it = 0; it < 8 && __any_sync(kFull, !fin); ++it) {
+    double sM = 0.0;
+    float nM = 0.f, nC = 0.f;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      if (cm >> k & 1u) {
+        const double dd = use32 ? 0.0 : dexact(k);
+        const bool lt = use32 ? d[k] < ph32 : dd < ph;
+        const bool cp = use32 ? d[k] <= ph32 - uf : dd <= ph - u;
+        if (lt) {
+          if (!cp) {
+            nM += 1.f;
+            sM += use32 ? dexact(k) : dd;
+          } else {
+            nC += 1.f;
+          }
+        }
+      }
+    }
+    nM = tsum<G>(nM);
+    nC = tsum<G>(nC);
+    sM = tsum<G>(sM);
+    use32 = false;
+    if (!fin) {
+      if (nM > 0.f) {
+        const double np = (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM;
+        fin = np == ph;
+        ph = np;
+      } else {
+        fin = true;  // flat F: any phi of the piece is a root (x is 0 or u there)
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < E; ++k) {
+    if (cm >> k & 1u) {
+      const double x = fmin(fmax(ph - dexact(k), 0.0), u);
+      if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + q + k * G, x, vs, b, q + k * G);
+    }
+  }
+}
+
+// Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
+// GEN: the kernel variant that solves box-cut and overflowing simplex groups inline (generic
+// path); otherwise overflowing simplex groups are deferred to deferred_kernel.
+template <int M, bool LAMS, bool WX, int LG, int E, bool GEN>
+__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
+                           const uint16_t* rel_s, uint16_t* cand_s) {
+  constexpr int G = 1 << LG;
+  constexpr int NG = 32 >> LG;
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;  // family f at sa + f*cap
+  const int gi = lane >> LG, q = lane & (G - 1);
+  const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
+  const int nrounds = (tl.nb + NG - 1) / NG;
+  const int kind = p.kind;
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const int bb = rd * NG + gi;
+    const bool active = bb < tl.nb;
+    const int b = tl.b0 + bb;
+    // block bounds: streamed into shared memory with the tile ({rel_0..rel_{nb-1}, nnz}), or
+    // read from global memory for tiles with many blocks
+    int start = 0, end = 0;
+    if (active) {
+      if (tl.rel_off >= 0) {
+        start = rel_s[bb];
+        end = rel_s[bb + 1];
+      } else {
+        start = (int)__ldg(p.blk_rel + b);
+        end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
+      }
+    }
+    const int len = end - start;
+    double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
+    if (p.vsq) {
+      if (active) {
+        vs = (double)__ldg(p.vsq + b);
+        ginv = C.invgamma * (double)__ldg(p.vinv + b);
+      }
+    }
+    // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family)
+    // and the magnitude |c| + sum_f |a_f lambda_f| bounding its rounding error.  Reads past the
+    // block end stay inside the stage buffers (tail padding); their dest is clamped to [0, J)
+    // and their s32 replaced by +inf.
+    const int32_t* sdp = sd + start + q;
+    const float* scp = sc + start + q;
+    const float* sap = sa + start + q;
+    const int lim = len - q;  // slot k of this lane is inside the block iff k*G < lim
+    float s32[E];
+    float lmin = kInfF, lmag = 0.f;
+#pragma unroll
+    for (int k = 0; k < E; ++k) {
+      const int j = (int)min((unsigned)sdp[k * G], Jm1);
+      const float cv = scp[k * G];
+      float sv = cv, mg = fabsf(cv);
+#pragma unroll
+      for (int f = 0; f < M; ++f) {
+        const float av = sap[f * cap + k * G], lv = C.lam(f, j);
+        sv = fmaf(av, lv, sv);
+        mg = fmaf(fabsf(av), fabsf(lv), mg);
+      }
+      const bool in = k * G < lim;
+      s32[k] = in ? sv : kInfF;
+      lmin = fminf(lmin, s32[k]);
+      if (in) lmag = fmaxf(lmag, mg);
+    }
+    // ---- candidates: entries that can have x > 0.  With one rounding per FMA,
+    // |fl32(s) - s| <= M 2^-24 (|c| + sum_f |a_f lambda_f|) = M 2^-24 mag per entry; the block
+    // slack 2^-22 (M+1) max(mag) covers the two errors of s_j - s_min with a 2x margin.
+    uint32_t cm = 0;
+    if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0: no coupling inside the block, x = clip(-s/gamma_i, 0, u)
+      const float slack = 2.3841858e-7f * (M + 1) * lmag;  // 2^-22 (M+1) mag (lane bound suffices)
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= slack) cm |= 1u << k;
+      if (!active) cm = 0;
+      while (cm) {
+        const int k = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const int e = q + k * G, ee = start + e;
+        const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), (double)p.u);
+        if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ee, x, vs, b, e);
+      }
+      continue;
+    }
+    const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);  // 2^-22 (M+1) max mag of the block
+    const double r = p.r;
+    if (GEN && kind == DL_PROJ_BOXCUT) {
+      // window above the K-th smallest s: active d < phi <= d_(K) + u, K = ceil(r/u)
+      const double u = p.u;
+      const int K = (int)ceil(r / u);
+      float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
+      uint32_t excl = 0;
+      bool sat = !active;
+      if (K <= 8) {
+        for (int rnd = 0; rnd < 8 && __any_sync(kFull, !sat); ++rnd) {
+          float ml = kInfF;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u)) ml = fminf(ml, s32[k]);
+          const float m = tmin<G>(ml);
+          float c = 0.f;
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (!(excl >> k & 1u) && s32[k] == m) {
+              c += 1.f;
+              excl |= 1u << k;
+            }
+          c = tsum<G>(c);
+          if (!sat) {
+            if (m == kInfF) {  // fewer than K entries: the sum cap cannot bind, all are candidates
+              sat = true;
+            } else {
+              cnt += c;
+              sk = m;
+              if (cnt >= (float)K) sat = true;
+            }
+          }
+        }
+      }
+      if (sat) {
+        const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] <= T) cm |= 1u << k;
+      } else {  // K > 8: every entry is a candidate
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+          if (s32[k] < kInfF) cm |= 1u << k;
+      }
+      if (!active) cm = 0;
+      if constexpr (GEN)
+        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, sat ? sk : 0.f,
+                                          s32);
+      continue;
+    }
+    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
+    const float ref = tmin<G>(lmin);
+    {
+      const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= T) cm |= 1u << k;
+    }
+    if (!active) cm = 0;
+    // ---- compaction: the group's candidates (entry indices) are packed into a per-warp
+    // shared list so that lane q of the group owns candidates q, q+G, q+2G, q+3G (<= 4 G).
+    const int nc = __popc(cm);
+    int incl = nc;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o, G);
+      if (q >= o) incl += v;
+    }
+    int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
+    if constexpr (GEN) {
+      if (!__all_sync(kFull, T <= 4 * G)) {
+        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
+        continue;
+      }
+    } else if (T > 4 * G) {  // defer this block to deferred_kernel (exact generic solve there)
+      if (q == 0) {
+        const int slot = atomicAdd(p.ctr + 6, 1);
+        if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, len};
+      }
+      cm = 0;
+      incl = 0;
+      T = 0;
+    }
+    {
+      uint32_t m = cm;
+      int o = gi * 4 * G + incl - nc;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        cand_s[o++] = (uint16_t)(start + q + k * G);
+      }
+    }
+    __syncwarp();
+    const int pmax = (__reduce_max_sync(kFull, (unsigned)T) + G - 1) >> LG;  // warp-uniform
+    const double refd = (double)ref;
+    const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
+    double d64[4];
+    int ei[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      d64[c] = kInfD;
+      ei[c] = -1;
+      if (c < pmax) {
+        const int idx = q + c * G;
+        if (idx < T) {
+          const int ee = cand_s[gi * 4 * G + idx];
+          d64[c] = (score_smem(C, sd, sc, sa, cap, ee) - refd) * ginv;
+          ei[c] = ee;
+        }
+      }
+    }
+    // Michelot in fp64 on the candidates for the root phi* of F(phi) = sum max(phi - d, 0) = r
+    // (every active entry is a candidate and phi* <= r + slack/gamma_i, so F over the candidates
+    // is F over the block there): start from all T candidates, phi = (r + sum_S d)/|S|,
+    // S = {d < phi}, until |S| is stable (1/|S| from a table, within 1 ulp).  The threshold is
+    // min(phi_free, phi*): theta = 0 exactly when phi_free <= phi* (F(phi_free) <= r).
+    double phi = 0.0;
+    bool done = !active || T <= 1;
+    {
+      double sl = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pmax && ei[c] >= 0) sl += d64[c];
+      const double sm = tsum<G>(sl);
+      if (!done) phi = (r + sm) * (T <= kRcpN ? c_rcp[T] : 1.0 / T);
+    }
+    int cprev = T;
+    for (int it = 0; it < 32 && __any_sync(kFull, !done); ++it) {
+      int cnt = 0;
+      double sl = 0.0;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (c < pmax) {
+          const bool in = d64[c] < phi;
+          cnt += tcount<G>(in, gmask);
+          if (in) sl += d64[c];
+        }
+      const double sm = tsum<G>(sl);
+      if (!done) {
+        if (cnt == cprev || cnt == 0) {
+          done = true;
+        } else {
+          cprev = cnt;
+          phi = (r + sm) * (cnt <= kRcpN ? c_rcp[cnt] : 1.0 / cnt);
+        }
+      }
+    }
+    if (active) {
+      const double ph = T == 1 ? phi_free : fmin(phi_free, phi);
+      const double cap_x = T == 1 ? r : kInfD;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < pmax && ei[c] >= 0) {
+          const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ei[c], x, vs, b, ei[c] - start);
+        }
+      }
+    }
+    __syncwarp();  // the candidate list is rewritten by the next round
+  }
+}
+
+template <int M, bool LAMS, bool WX, bool GEN>
+__device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
+                                               const uint16_t* rel_s, uint16_t* cand_s) {
+  switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
+    case 1:
+    case 2:
+    case 3: small_tile<M, LAMS, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+  }
+}
+
+template <int M, bool LAMS, bool WX, bool GEN>
+__global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_constant__ GradArgs p) {
+  extern __shared__ __align__(128) char smem[];
+  SmemHead* head = reinterpret_cast<SmemHead*>(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* after_head = smem + 2048;
+  float* lam_s = nullptr;
+  size_t lam_bytes = 0;
+  if constexpr (LAMS) {
+    lam_s = reinterpret_cast<float*>(after_head);
+    lam_bytes = ((size_t)M * p.J * 4 + 127) / 128 * 128;
+    const int n = M * p.J;
+    for (int i = threadIdx.x; i < n; i += kThreads) lam_s[i] = __ldg(p.lam + i);
+  }
+  char* tilebuf = after_head + lam_bytes;
+  const uint32_t stage_bytes = (uint32_t)p.tile_cap * (8u + 4u * M);
+  if (lane == 0) {
+    mbar_init(&head->mbar[warp][0], 1);
+    mbar_init(&head->mbar[warp][1], 1);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
+  Ctx<M, LAMS, WX> C(p, lam_s, gamma);
+
+  // ---- phase 1: big blocks, groups of 16 / 8 / 4 / 2 warps; barrier ids unique per group
+  for (int ph = 0; ph < kNumBigPhases; ++ph) {
+    if (p.ph_begin[ph] == p.ph_begin[ph + 1]) continue;
+    BigGroup g;
+    g.gw = 16 >> ph;
+    g.G = g.gw * 32;
+    const int grp = warp / g.gw;
+    g.warp0 = grp * g.gw;
+    g.gtid = (warp - g.warp0) * 32 + lane;
+    g.bar = (1 << ph) + grp;  // phase 0: 1, phase 1: 2-3, phase 2: 4-7, phase 3: 8-15
+    g.lane = lane;
+    g.warp = warp;
+    g.head = head;
+    // scratch: this group's warps' tile buffers (doubles), else a global slice
+    double* scr_smem = reinterpret_cast<double*>(tilebuf + (size_t)g.warp0 * 2 * stage_bytes);
+    const int scr_cap = (int)((size_t)g.gw * 2 * stage_bytes / 8);
+    for (;;) {
+      if (g.gtid == 0) head->slot[g.bar] = atomicAdd(p.ctr + ph, 1) + p.ph_begin[ph];
+      g.sync();
+      const int ti = head->slot[g.bar];
+      if (ti >= p.ph_begin[ph + 1]) break;
+      const Tile tl = p.tiles[ti];
+      double* scr = tl.nnz <= scr_cap ? scr_smem : p.gscratch + (size_t)blockIdx.x * p.gscratch_per_cta;
+      big_block<M, LAMS, WX>(C, g, tl, scr);
+    }
+  }
+
+  // ---- phase 2: small tiles.  Each warp runs its own asynchronous stream: tiles are claimed
+  // in chunks of kChunk (one atomic per chunk, claimed a chunk ahead); the chunk's tile
+  // descriptors arrive by a 128-B bulk copy into a shared slot; every tile's dest / c / a_k
+  // arrays and its block offsets arrive by bulk copies into a double-buffered stage.  No
+  // global load sits on the critical path of a tile.
+  {
+    constexpr int kChunk = 4;
+    const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
+    char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
+    char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMetaBytes;
+    const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
+    const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // [128] candidate list
+    uint64_t* bars = head->mbar[warp];
+    uint64_t* dbars = head->mbar_desc[warp];
+    if (lane == 0) {
+      mbar_init(&dbars[0], 1);
+      mbar_init(&dbars[1], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    // lane 0 claims a chunk; the value is broadcast only when it is used (a chunk later), so
+    // the atomic's latency is not waited on
+    auto grab = [&]() {
+      int c = 0;
+      if (lane == 0) c = atomicAdd(p.ctr + kNumBigPhases, 1);
+      return c;
+    };
+    auto first_of = [&](int raw) { return s_begin + kChunk * __shfl_sync(kFull, raw, 0); };
+    auto issue_desc = [&](int first, int slot) {
+      if (lane == 0 && first < s_end) {
+        fence_proxy_async();
+        mbar_expect_tx(&dbars[slot], kChunk * (uint32_t)sizeof(Tile));
+        tma_bulk_g2s(meta + slot * 128, p.tiles + first, kChunk * (uint32_t)sizeof(Tile), &dbars[slot]);
+      }
+    };
+    auto issue_tile = [&](const Tile& t, int st) {
+      if (lane == 0) {
+        const uint32_t n4 = (uint32_t)((t.nnz + kAlign - 1) / kAlign * kAlign);
+        const uint32_t bytes = n4 * 4u;
+        const uint32_t rbytes = t.rel_off >= 0 ? (uint32_t)((2 * (t.nb + 1) + 15) & ~15) : 0u;
+        char* dst = mybuf + (size_t)st * stage_bytes;
+        fence_proxy_async();
+        mbar_expect_tx(&bars[st], bytes * (2u + M) + rbytes);
+        tma_bulk_g2s(dst, p.dest + t.off, bytes, &bars[st]);
+        tma_bulk_g2s(dst + (size_t)p.tile_cap * 4, p.c + t.off, bytes, &bars[st]);
+#pragma unroll
+        for (int f = 0; f < M; ++f)
+          tma_bulk_g2s(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st]);
+        if (rbytes) tma_bulk_g2s(meta + 256 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
+      }
+    };
+    uint32_t phase = 0u, dphase = 0u;  // mbarrier parities, bit s for slot s (kept in registers)
+    int c0 = first_of(grab()), c1 = first_of(grab());
+    int ds = 0;  // descriptor slot of chunk c0
+    issue_desc(c0, 0);
+    issue_desc(c1, 1);
+    int c2raw = grab();
+    int pos = 0, st = 0;
+    Tile t{};
+    bool have = c0 < s_end;
+    if (have) {
+      mbar_wait(&dbars[0], dphase & 1u);
+      dphase ^= 1u;
+      t = dslot[0];
+      issue_tile(t, 0);
+    }
+    while (have) {
+      // descriptor of the next tile: same chunk, or the first of the next chunk
+      Tile tn{};
+      bool nhave;
+      const bool same = pos + 1 < kChunk && c0 + pos + 1 < s_end;
+      if (same) {
+        tn = dslot[ds * kChunk + pos + 1];
+        nhave = true;
+      } else {
+        nhave = c1 < s_end;
+        if (nhave) {
+          mbar_wait(&dbars[ds ^ 1], (dphase >> (ds ^ 1)) & 1u);
+          dphase ^= 1u << (ds ^ 1);
+          tn = dslot[(ds ^ 1) * kChunk];
+        }
+      }
+      if (nhave) issue_tile(tn, st ^ 1);
+      mbar_wait(&bars[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+      small_dispatch<M, LAMS, WX, GEN>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot);
+      __syncwarp();
+      if (same) {
+        ++pos;
+      } else {  // chunk c0 done: its descriptor slot takes chunk c2
+        const int c2 = first_of(c2raw);
+        __syncwarp();
+        issue_desc(c2, ds);
+        c0 = c1;
+        c1 = c2;
+        ds ^= 1;
+        pos = 0;
+        c2raw = c1 < s_end ? grab() : (s_end - s_begin) / kChunk + 1;  // past the end
+      }
+      t = tn;
+      have = nhave;
+      st ^= 1;
+    }
+  }
+
+  // ---- objective scalars: warp reduce, one fp64 atomic per warp
+  double cx = C.cx, rg = C.reg;
+  float nx = C.nx;
+  for (int o = 16; o > 0; o >>= 1) {
+    cx += __shfl_xor_sync(kFull, cx, o);
+    rg += __shfl_xor_sync(kFull, rg, o);
+    nx += __shfl_xor_sync(kFull, nx, o);
+  }
+  if (lane == 0) {
+    const size_t n = (size_t)M * p.J;
+    atomicAdd(p.acc + n + 0, cx);
+    atomicAdd(p.acc + n + 1, rg);
+    atomicAdd(p.acc + n + 2, (double)nx);
+  }
+}
+
+// Deferred simplex blocks (groups whose candidates overflowed the register fast path): one
+// warp per block, staged from global memory into shared memory, generic exact solve.
+template <int M, bool WX>
+__global__ void __launch_bounds__(256) deferred_kernel(const __grid_constant__ GradArgs p) {
+  constexpr int kW = 8;
+  constexpr int kStage = 256;  // entries (blocks here are < 256 long)
+  extern __shared__ __align__(128) char dsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  char* stage = dsm + (size_t)warp * kStage * (8 + 4 * M);
+  int32_t* sd = reinterpret_cast<int32_t*>(stage);
+  float* sc = reinterpret_cast<float*>(stage) + kStage;
+  float* sa = sc + kStage;
+  const int n = min(p.ctr[6], p.defer_cap);
+  const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
+  GradArgs pl = p;
+  pl.tile_cap = kStage;
+  Ctx<M, false, WX> C(pl, nullptr, gamma);
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  for (int i = blockIdx.x * kW + warp; i < n; i += gridDim.x * kW) {
+    const DeferEntry de = p.defer[i];
+    for (int e = lane; e < kStage; e += 32) {
+      const bool v = e < de.len;
+      sd[e] = v ? __ldg(p.dest + de.off + e) : 0;
+      sc[e] = v ? __ldg(p.c + de.off + e) : 0.f;
+#pragma unroll
+      for (int f = 0; f < M; ++f) sa[f * kStage + e] = v ? __ldg(p.a + f * p.a_stride + de.off + e) : 0.f;
+    }
+    __syncwarp();
+    double vs = 1.0, ginv = C.invgamma;
+    if (p.vsq) {
+      vs = (double)__ldg(p.vsq + de.b);
+      ginv = C.invgamma * (double)__ldg(p.vinv + de.b);
+    }
+    float s32[8];
+    float lmin = kInfF, lmag = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int e = lane + 32 * k;
+      const int j = (int)min((unsigned)sd[e], Jm1);
+      float sv = sc[e], mg = fabsf(sc[e]);
+#pragma unroll
+      for (int f = 0; f < M; ++f) {
+        const float av = sa[f * kStage + e], lv = C.lam(f, j);
+        sv = fmaf(av, lv, sv);
+        mg = fmaf(fabsf(av), fabsf(lv), mg);
+      }
+      s32[k] = e < de.len ? sv : kInfF;
+      lmin = fminf(lmin, s32[k]);
+      if (e < de.len) lmag = fmaxf(lmag, mg);
+    }
+    const float ref = tmin<32>(lmin);
+    const float slack = 2.3841858e-7f * (M + 1) * tmax<32>(lmag);
+    const float T = ref + ((float)(p.r * gamma * vs) * 1.000001f + slack);
+    uint32_t cm = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (s32[k] <= T) cm |= 1u << k;
+    // the block's entries sit at [0, len) of the warp's stage; orig_off / x_out use de.b
+    generic_round<M, false, WX, 5, 8>(C, sd, sc, sa, kStage, lane, 0, true, de.b, vs, ginv, cm, ref, s32);
+    __syncwarp();
+  }
+  double cx = C.cx, rg = C.reg;
+  float nx = C.nx;
+  for (int o = 16; o > 0; o >>= 1) {
+    cx += __shfl_xor_sync(kFull, cx, o);
+    rg += __shfl_xor_sync(kFull, rg, o);
+    nx += __shfl_xor_sync(kFull, nx, o);
+  }
+  if (lane == 0 && nx > 0.f) {
+    const size_t nn = (size_t)M * p.J;
+    atomicAdd(p.acc + nn + 0, cx);
+    atomicAdd(p.acc + nn + 1, rg);
+    atomicAdd(p.acc + nn + 2, (double)nx);
+  }
+}
+
+template <int M, bool LAMS, bool WX, bool GEN>
+cudaError_t launch_t(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  auto k = fused_grad_kernel<M, LAMS, WX, GEN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k<<<ctas, kThreads, smem, s>>>(a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || GEN || !a.defer) return e;
+  const size_t dsmem = (size_t)8 * 256 * (8 + 4 * M);
+  auto dk = deferred_kernel<M, WX>;
+  e = cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
+  if (e != cudaSuccess) return e;
+  dk<<<ctas, 256, dsmem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int M>
+cudaError_t launch_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  const bool wx = a.x_out != nullptr;
+  if (a.kind == DL_PROJ_BOXCUT) {
+    if (a.lam_smem)
+      return wx ? launch_t<M, true, true, true>(a, ctas, smem, s) : launch_t<M, true, false, true>(a, ctas, smem, s);
+    return wx ? launch_t<M, false, true, true>(a, ctas, smem, s) : launch_t<M, false, false, true>(a, ctas, smem, s);
+  }
+  if (a.lam_smem)
+    return wx ? launch_t<M, true, true, false>(a, ctas, smem, s) : launch_t<M, true, false, false>(a, ctas, smem, s);
+  return wx ? launch_t<M, false, true, false>(a, ctas, smem, s) : launch_t<M, false, false, false>(a, ctas, smem, s);
+}
+
+}  // namespace
+
+// one translation unit per family count (grad_m<M>.cu), compiled in parallel
+template <>
+cudaError_t launch_fused_grad_m<DL_GRAD_M>(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  return launch_m<DL_GRAD_M>(a, ctas, smem, s);
+}
+
+}  // namespace dl

@@ -107,6 +107,8 @@ struct GradArgs {
 };
 
 cudaError_t launch_fused_grad(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
+template <int M>
+cudaError_t launch_fused_grad_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
 
 struct StepArgs {
   int32_t n;               // m*J
