@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libdualip.so")
+LIB_PATH = os.environ.get("DUALIP_LIB") or os.path.join(HERE, "lib", "libdualip.so")  # override: A/B diagnostics
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2603_04621_b200.build` "

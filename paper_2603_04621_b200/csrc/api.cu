@@ -424,7 +424,21 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
   la.a_out = p->d_a;
   la.vsq_out = p->d_vsq;
   la.vinv_out = p->d_vinv;
+  la.J = p->J;
+  int32_t* d_bad = nullptr;
+  if ((s = dev_alloc(p, &d_bad, 1))) return fail(s);
+  CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int32_t), p->stream));
+  la.bad = d_bad;
   CUDA_TRY(launch_build_layout(la, p->stream));
+  {
+    int32_t bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, p->stream));
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    if (bad) {
+      set_error("dl_problem_create: a dest index is outside [0, num_dests)");
+      return fail(DL_ERR_INVALID);
+    }
+  }
   CUDA_TRY(launch_jacobi_diag(nullptr, p->d_D, (int32_t)MJ, p->stream));
   CUDA_TRY(launch_jacobi_diag(nullptr, p->d_Dones, (int32_t)MJ, p->stream));
   // magnitude bounds for the fp32 candidate filter: max|c|, max|a_f|
@@ -600,8 +614,21 @@ dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm) {
         (s = dev_alloc(p, &p->d_mu, n)) || (s = dev_alloc(p, &p->d_st, 1)))
       return s;
   }
+  // the captured solve graph bakes in the history buffer and the Jacobi diagonal: rebuild it
+  if (p->graph) {
+    CUDA_TRY(cudaStreamSynchronize(p->stream));
+    cudaGraphExecDestroy(p->graph);
+    p->graph = nullptr;
+  }
   const int64_t cap = prm->history_cap > 0 ? prm->history_cap : 65536;
   if (cap != p->hist_cap) {
+    if (p->d_hist) {
+      CUDA_TRY(cudaStreamSynchronize(p->stream));
+      cudaFree(p->d_hist);
+      p->allocs.erase(std::find(p->allocs.begin(), p->allocs.end(), (void*)p->d_hist));
+      p->device_bytes -= std::max<int64_t>(p->hist_cap, 1) * (int64_t)sizeof(dl_iter_record);
+      p->d_hist = nullptr;
+    }
     dl_status s = dev_alloc(p, &p->d_hist, cap);
     if (s) return s;
     p->hist_cap = cap;

@@ -172,7 +172,8 @@ __device__ __forceinline__ void solver_update(Solver& S, double r, double u, con
 struct SmemHead {
   uint64_t mbar[kWarps][2];       // data stages (tile arrays + block offsets)
   uint64_t mbar_desc[kWarps][2];  // descriptor-chunk slots
-  double red[2][kWarps][4];
+  double red[2][kWarps][3];
+  double rcp[kRcpN + 1];          // 1/n, n = 0..kRcpN (copied from c_rcp: divergent n, no constant-bank replays)
   int32_t slot[16];
 };
 static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
@@ -380,7 +381,14 @@ __device__ __forceinline__ float capsumf(float u, float nC) { return nC > 0.f ? 
 // entry near a breakpoint is O(max(r, u)) in this frame; a safeguarded Newton in fp32 (Illinois
 // secant / bisection fallback) finds the partition, then Newton steps in fp64 on the exact
 // partition (exact d recomputed from shared memory) give phi = (r - u|C| + sum_M d)/|M|.
-template <int M, bool LAMS, bool WX, int LG, int E>
+// Slot k of lane q (group of G lanes) -> block-relative entry: strided (q + k G), or, in the
+// float4 layout of the small-tile path, component k&3 of the lane's (k>>2)-th float4 q + (k>>2) G.
+template <int LG, bool V4>
+__device__ __forceinline__ int slot_entry(int q, int k) {
+  return V4 ? 4 * (q + (k >> 2) * (1 << LG)) + (k & 3) : q + k * (1 << LG);
+}
+
+template <int M, bool LAMS, bool WX, int LG, int E, bool V4>
 __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
                                               const float* sa, int cap, int q, int start, bool active, int b,
                                               double vs, double ginv, uint32_t cm, float ref, float (&d)[E]) {
@@ -390,7 +398,7 @@ __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t
   const double r = p.r, u = p.u;
   const float rf = p.r, uf = p.u;
   const double refd = (double)ref;
-  auto dexact = [&](int k) { return (score_smem(C, sd, sc, sa, cap, start + q + k * G) - refd) * ginv; };
+  auto dexact = [&](int k) { return (score_smem(C, sd, sc, sa, cap, start + slot_entry<LG, V4>(q, k)) - refd) * ginv; };
   // d in fp32 from the caller's fp32 scores (in place): only the partition search uses it; the
   // fp64 Newton steps below re-derive exact d from shared memory and settle any boundary entry
   const float ginvf = (float)ginv;
@@ -523,17 +531,21 @@ __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t
   for (int k = 0; k < E; ++k) {
     if (cm >> k & 1u) {
       const double x = fmin(fmax(ph - dexact(k), 0.0), u);
-      if (x > 0.0) emit_smem(C, sd, sc, sa, cap, start + q + k * G, x, vs, b, q + k * G);
+      if (x > 0.0) {
+        const int e = slot_entry<LG, V4>(q, k);
+        emit_smem(C, sd, sc, sa, cap, start + e, x, vs, b, e);
+      }
     }
   }
 }
 
-// Short blocks of one tile, G = 2^LG lanes per block, E entries per lane (E G > max length).
+// Short blocks of one tile (buckets < kBigBucket), G = 2^LG lanes per block, NG = 32/G blocks
+// per round, E entries (slots) per lane (E G > every length of the bucket).
 // GEN: the kernel variant that solves box-cut and overflowing simplex groups inline (generic
 // path); otherwise overflowing simplex groups are deferred to deferred_kernel.
 template <int M, bool LAMS, bool WX, int LG, int E, bool GEN>
 __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
-                           const uint16_t* rel_s, uint16_t* cand_s) {
+                           const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
   const GradArgs& p = C.p;
@@ -545,13 +557,12 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   const uint32_t gmask = (G == 32 ? kFull : ((1u << G) - 1u)) << (gi * G);
   const int nrounds = (tl.nb + NG - 1) / NG;
   const int kind = p.kind;
-  const unsigned Jm1 = (unsigned)p.J - 1u;
   for (int rd = 0; rd < nrounds; ++rd) {
     const int bb = rd * NG + gi;
     const bool active = bb < tl.nb;
     const int b = tl.b0 + bb;
-    // block bounds: streamed into shared memory with the tile ({rel_0..rel_{nb-1}, nnz}), or
-    // read from global memory for tiles with many blocks
+    // block bounds: streamed into shared memory with the tile ({rel_0..rel_{nb-1},
+    // nnz}), or read from global memory for tiles with many blocks
     int start = 0, end = 0;
     if (active) {
       if (tl.rel_off >= 0) {
@@ -562,7 +573,6 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
       }
     }
-    const int len = end - start;
     double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
     if (p.vsq) {
       if (active) {
@@ -570,38 +580,36 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         ginv = C.invgamma * (double)__ldg(p.vinv + b);
       }
     }
-    // ---- fp32 pass over every entry: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family)
-    // and the magnitude |c| + sum_f |a_f lambda_f| bounding its rounding error.  Reads past the
-    // block end stay inside the stage buffers (tail padding); their dest is clamped to [0, J)
-    // and their s32 replaced by +inf.
-    const int32_t* sdp = sd + start + q;
-    const float* scp = sc + start + q;
-    const float* sap = sa + start + q;
-    const int lim = len - q;  // slot k of this lane is inside the block iff k*G < lim
+    // ---- fp32 pass: s32 = fl(c + sum_f a_f lambda_f) (one FMA per family) for every slot; slot k
+    // of lane q is entry q + k G of the block (consecutive lanes read consecutive words: no bank
+    // conflicts on the stage); slots past the block end are +inf.
     float s32[E];
     float lmin = kInfF, lmag = 0.f;
+    {
+      const int lim = (end - start) - q;
 #pragma unroll
-    for (int k = 0; k < E; ++k) {
-      const int j = (int)min((unsigned)sdp[k * G], Jm1);
-      const float cv = scp[k * G];
-      float sv = cv, mg = fabsf(cv);
+      for (int k = 0; k < E; ++k) {
+        const int ee = start + q + k * G;
+        const bool in = k * G < lim;
+        const int j = in ? sd[ee] : 0;  // reads past the tile stay inside shared memory (tail pad)
+        float sv = in ? sc[ee] : kInfF, mg = fabsf(sv);
 #pragma unroll
-      for (int f = 0; f < M; ++f) {
-        const float av = sap[f * cap + k * G], lv = C.lam(f, j);
-        sv = fmaf(av, lv, sv);
-        mg = fmaf(fabsf(av), fabsf(lv), mg);
+        for (int f = 0; f < M; ++f) {
+          const float a_ = in ? sa[f * cap + ee] : 0.f, lv = C.lam(f, j);
+          sv = fmaf(a_, lv, sv);
+          if constexpr (M > 1) mg = fmaf(fabsf(a_), fabsf(lv), mg);
+        }
+        s32[k] = sv;
+        lmin = fminf(lmin, sv);
+        if constexpr (M > 1) lmag = sv < kInfF ? fmaxf(lmag, mg) : lmag;
       }
-      const bool in = k * G < lim;
-      s32[k] = in ? sv : kInfF;
-      lmin = fminf(lmin, s32[k]);
-      if (in) lmag = fmaxf(lmag, mg);
     }
-    // ---- candidates: entries that can have x > 0.  With one rounding per FMA,
-    // |fl32(s) - s| <= M 2^-24 (|c| + sum_f |a_f lambda_f|) = M 2^-24 mag per entry; the block
-    // slack 2^-22 (M+1) max(mag) covers the two errors of s_j - s_min with a 2x margin.
+    // ---- candidates: entries that can have x > 0.  M = 1: one rounding, |fl(s) - s| <= 2^-24 |s|;
+    // M > 1: |fl32(s) - s| <= M 2^-24 (|c| + sum_f |a_f lambda_f|) = M 2^-24 mag per entry.
     uint32_t cm = 0;
     if (kind == DL_PROJ_BOX) {  // x > 0  iff  s < 0: no coupling inside the block, x = clip(-s/gamma_i, 0, u)
-      const float slack = 2.3841858e-7f * (M + 1) * lmag;  // 2^-22 (M+1) mag (lane bound suffices)
+      // M = 1: the rounding keeps the sign (s < 0 => fl(s) <= 0); M > 1: lane bound 2^-22 (M+1) mag
+      const float slack = M == 1 ? 0.f : 2.3841858e-7f * (M + 1) * lmag;
 #pragma unroll
       for (int k = 0; k < E; ++k)
         if (s32[k] <= slack) cm |= 1u << k;
@@ -609,15 +617,15 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       while (cm) {
         const int k = __ffs(cm) - 1;
         cm &= cm - 1;
-        const int e = q + k * G, ee = start + e;
+        const int e = slot_entry<LG, false>(q, k), ee = start + e;
         const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), (double)p.u);
         if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ee, x, vs, b, e);
       }
       continue;
     }
-    const float slack = 2.3841858e-7f * (M + 1) * tmax<G>(lmag);  // 2^-22 (M+1) max mag of the block
     const double r = p.r;
     if (GEN && kind == DL_PROJ_BOXCUT) {
+      const float slack_m = M == 1 ? 0.f : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
       // window above the K-th smallest s: active d < phi <= d_(K) + u, K = ceil(r/u)
       const double u = p.u;
       const int K = (int)ceil(r / u);
@@ -651,7 +659,10 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         }
       }
       if (sat) {
-        const float T = sk + ((float)(u * C.gamma * vs) * 1.000001f + slack);
+        // slack as for the simplex with ref = s_(K) and the window gamma_i u
+        const float gu = (float)(u * C.gamma * vs);
+        const float slack = M == 1 ? 4.7683716e-7f * (fabsf(sk) + gu) : slack_m;
+        const float T = sk + (gu * 1.000001f + slack);
 #pragma unroll
         for (int k = 0; k < E; ++k)
           if (s32[k] <= T) cm |= 1u << k;
@@ -662,20 +673,24 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       }
       if (!active) cm = 0;
       if constexpr (GEN)
-        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, sat ? sk : 0.f,
-                                          s32);
+        generic_round<M, LAMS, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm,
+                                                sat ? sk : 0.f, s32);
       continue;
     }
-    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r
+    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r.  The block slack covers the two
+    // roundings of s_j - s_min and of the threshold sum: M = 1: 2^-21 (|ref| + gamma_i r)
+    // (>= 2.6x the bound 2^-24 (3 |ref| + 2 gamma_i r)); M > 1: 2^-22 (M+1) max mag (2x margin).
     const float ref = tmin<G>(lmin);
+    const float gr = (float)(r * C.gamma * vs);
+    const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
     {
-      const float T = ref + ((float)(r * C.gamma * vs) * 1.000001f + slack);
+      const float T = ref + (gr * 1.000001f + slack);
 #pragma unroll
       for (int k = 0; k < E; ++k)
         if (s32[k] <= T) cm |= 1u << k;
     }
     if (!active) cm = 0;
-    // ---- compaction: the group's candidates (entry indices) are packed into a per-warp
+    // ---- compaction: the group's candidates (tile entry indices) are packed into a per-warp
     // shared list so that lane q of the group owns candidates q, q+G, q+2G, q+3G (<= 4 G).
     const int nc = __popc(cm);
     int incl = nc;
@@ -687,13 +702,13 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
     if constexpr (GEN) {
       if (!__all_sync(kFull, T <= 4 * G)) {
-        generic_round<M, LAMS, WX, LG, E>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
+        generic_round<M, LAMS, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
         continue;
       }
     } else if (T > 4 * G) {  // defer this block to deferred_kernel (exact generic solve there)
       if (q == 0) {
         const int slot = atomicAdd(p.ctr + 6, 1);
-        if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, len};
+        if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, end - start};
       }
       cm = 0;
       incl = 0;
@@ -705,7 +720,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
-        cand_s[o++] = (uint16_t)(start + q + k * G);
+        cand_s[o++] = (uint16_t)(start + slot_entry<LG, false>(q, k));
       }
     }
     __syncwarp();
@@ -730,8 +745,8 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     // Michelot in fp64 on the candidates for the root phi* of F(phi) = sum max(phi - d, 0) = r
     // (every active entry is a candidate and phi* <= r + slack/gamma_i, so F over the candidates
     // is F over the block there): start from all T candidates, phi = (r + sum_S d)/|S|,
-    // S = {d < phi}, until |S| is stable (1/|S| from a table, within 1 ulp).  The threshold is
-    // min(phi_free, phi*): theta = 0 exactly when phi_free <= phi* (F(phi_free) <= r).
+    // S = {d < phi}, until |S| is stable (1/|S| from a shared table, within 1 ulp).  The threshold
+    // is min(phi_free, phi*): theta = 0 exactly when phi_free <= phi* (F(phi_free) <= r).
     double phi = 0.0;
     bool done = !active || T <= 1;
     {
@@ -740,7 +755,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       for (int c = 0; c < 4; ++c)
         if (c < pmax && ei[c] >= 0) sl += d64[c];
       const double sm = tsum<G>(sl);
-      if (!done) phi = (r + sm) * (T <= kRcpN ? c_rcp[T] : 1.0 / T);
+      if (!done) phi = (r + sm) * (T <= kRcpN ? rcp_s[T] : 1.0 / T);
     }
     int cprev = T;
     for (int it = 0; it < 32 && __any_sync(kFull, !done); ++it) {
@@ -759,7 +774,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
           done = true;
         } else {
           cprev = cnt;
-          phi = (r + sm) * (cnt <= kRcpN ? c_rcp[cnt] : 1.0 / cnt);
+          phi = (r + sm) * (cnt <= kRcpN ? rcp_s[cnt] : 1.0 / cnt);
         }
       }
     }
@@ -780,16 +795,16 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
 
 template <int M, bool LAMS, bool WX, bool GEN>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
-                                               const uint16_t* rel_s, uint16_t* cand_s) {
-  switch (tl.bucket) {  // (G, E): G E >= 2^t - 1 > every length of bucket t
+                                               const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
+  switch (tl.bucket) {  // (LG, E): E 2^LG > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 6: small_tile<M, LAMS, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
-    case 7: small_tile<M, LAMS, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
-    default: small_tile<M, LAMS, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s); break;
+    case 3: small_tile<M, LAMS, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 4: small_tile<M, LAMS, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 5: small_tile<M, LAMS, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 6: small_tile<M, LAMS, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 7: small_tile<M, LAMS, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    default: small_tile<M, LAMS, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
   }
 }
 
@@ -813,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     mbar_init(&head->mbar[warp][0], 1);
     mbar_init(&head->mbar[warp][1], 1);
   }
+  for (int i = threadIdx.x; i <= kRcpN; i += kThreads) head->rcp[i] = c_rcp[i];
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
 
@@ -932,7 +948,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (nhave) issue_tile(tn, st ^ 1);
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
-      small_dispatch<M, LAMS, WX, GEN>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot);
+      small_dispatch<M, LAMS, WX, GEN>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,
+                                       head->rcp);
       __syncwarp();
       if (same) {
         ++pos;
@@ -1016,17 +1033,19 @@ __global__ void __launch_bounds__(256) deferred_kernel(const __grid_constant__ G
       }
       s32[k] = e < de.len ? sv : kInfF;
       lmin = fminf(lmin, s32[k]);
-      if (e < de.len) lmag = fmaxf(lmag, mg);
+      if (s32[k] < kInfF) lmag = fmaxf(lmag, mg);  // padding (c = +inf) excluded
     }
+    // candidate slack as in small_tile
     const float ref = tmin<32>(lmin);
-    const float slack = 2.3841858e-7f * (M + 1) * tmax<32>(lmag);
-    const float T = ref + ((float)(p.r * gamma * vs) * 1.000001f + slack);
+    const float gr = (float)(p.r * gamma * vs);
+    const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<32>(lmag);
+    const float T = ref + (gr * 1.000001f + slack);
     uint32_t cm = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if (s32[k] <= T) cm |= 1u << k;
     // the block's entries sit at [0, len) of the warp's stage; orig_off / x_out use de.b
-    generic_round<M, false, WX, 5, 8>(C, sd, sc, sa, kStage, lane, 0, true, de.b, vs, ginv, cm, ref, s32);
+    generic_round<M, false, WX, 5, 8, false>(C, sd, sc, sa, kStage, lane, 0, true, de.b, vs, ginv, cm, ref, s32);
     __syncwarp();
   }
   double cx = C.cx, rg = C.reg;

@@ -164,6 +164,8 @@ struct LayoutArgs {
   float* a_out;
   float* vsq_out;
   float* vinv_out;
+  int32_t J;
+  int32_t* bad;  // set to 1 if a dest index is outside [0, J)
 };
 cudaError_t launch_build_layout(const LayoutArgs& a, cudaStream_t s);
 

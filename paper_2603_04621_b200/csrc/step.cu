@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kStepThreads) slack_kernel(const float* lam, i
 __global__ void absmax_kernel(const float* x, int64_t n, unsigned int* out) {
   float v = 0.f;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v = fmaxf(v, fabsf(x[i]));
+    if (fabsf(x[i]) < __int_as_float(0x7f800000)) v = fmaxf(v, fabsf(x[i]));  // layout padding is +inf
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(v));  // v >= 0: uint order = float order
 }
@@ -232,10 +232,13 @@ __global__ void build_layout_kernel(const LayoutArgs a) {
     const int64_t s0 = a.row_ptr[i], len = a.row_ptr[i + 1] - s0;
     const int64_t d0 = a.blk_off[b];
     for (int64_t e = lane; e < len; e += 32) {
-      a.dest_out[d0 + e] = a.dest[s0 + e];
+      const int32_t j = a.dest[s0 + e];
+      if ((uint32_t)j >= (uint32_t)a.J) *a.bad = 1;
+      a.dest_out[d0 + e] = j;
       a.c_out[d0 + e] = a.c[s0 + e];
       for (int f = 0; f < a.m; ++f) a.a_out[f * a.a_stride_out + d0 + e] = a.a[f * a.nnz + s0 + e];
     }
+
     if (lane == 0 && a.vsq_out) {
       const float v = a.v[i];
       a.vsq_out[b] = v * v;

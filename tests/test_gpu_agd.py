@@ -71,3 +71,21 @@ def test_solve_converges_like_oracle():
         return int(np.flatnonzero(ghat - best <= 1e-3 * abs(ghat))[0])
     a, b = first(h["g"]), first(tr.g)
     assert abs(a - b) <= max(3, 0.02 * b), (a, b)
+
+
+def test_reinit_rebuilds_the_solve_graph():
+    """dl_agd_init after a graph-captured dl_solve (new history capacity, Jacobi switched on) must
+    restart from lambda = 0 with the new buffers: the second run equals a fresh one."""
+    inst = generate(CONFIGS["tiny"])
+    cfg = AgdConfig(gamma0=0.01)
+    gp = MatchingProblem.from_instance(inst)
+    gp.agd_init(gamma0=0.01, use_jacobi=False, max_step=1e-3, init_step=1e-5, history_cap=64)
+    gp.solve(40)                                   # captures the solve graph
+    gp.set_jacobi(gp.row_sqnorms())
+    gp.agd_init(gamma0=0.01, use_jacobi=True, max_step=1e-3, init_step=1e-5, history_cap=500)
+    gp.solve(100)
+    h = gp.history()
+    gp.close()
+    tr = agd(Problem.from_instance(inst), 100, cfg)
+    assert h.size == 100
+    np.testing.assert_allclose(h["g"], tr.g, rtol=1e-6)
