@@ -355,7 +355,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 8 * (n + 4)},
-            "gpu_launches": 3 * args.steps,  # per step: fused_grad_kernel, deferred_kernel, agd_step_kernel
+            "gpu_launches": 4 * args.steps,  # per step: fused_grad, deferred, agd_reduce, agd_update kernels
             "clocks": clk.summary(),
             "time_to_gap": gap,
             "setup": {"generate_s": t_gen, "tile_cap": gp.info["tile_cap"], "tiles": gp.info["num_tiles"],

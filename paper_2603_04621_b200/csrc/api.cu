@@ -79,8 +79,9 @@ struct dl_problem {
   DeferEntry* d_defer = nullptr;
   int32_t defer_cap = 0;
   int64_t gscratch_per_cta = 0;
-  float cmax = 0.f, amax[4] = {0.f, 0.f, 0.f, 0.f};
-  float* d_slack = nullptr;  // [2]: 0 standalone path, 1 solver path
+  double* d_step_part = nullptr;  // AGD step: per-CTA partials, completion counter, eta/beta
+  int32_t* d_step_done = nullptr;
+  double* d_step_scal = nullptr;
   // work
   double* d_acc = nullptr;   // [MJ + 4]
   int32_t* d_ctr = nullptr;  // [8]
@@ -168,10 +169,8 @@ void free_all(dl_problem* p) {
   if (p->own_stream && p->stream) cudaStreamDestroy(p->stream);
 }
 
-GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, double gamma_val, float* x_out,
-                   const float* slack) {
+GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, double gamma_val, float* x_out) {
   GradArgs a{};
-  a.slack = slack;
   a.dest = p->d_dest;
   a.c = p->d_c;
   a.a = p->d_a;
@@ -211,12 +210,7 @@ dl_status run_grad(dl_problem* p, const float* lam, const double* gamma_ptr, dou
     CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, 8 * sizeof(int32_t), p->stream));
   }
   if (p->plan.tiles.empty()) return DL_OK;
-  const float* slack = p->d_slack + 1;  // solver path: written by the step kernel
-  if (zero_first) {                      // standalone path: bound for this lambda
-    CUDA_TRY(launch_slack(lam, p->M, p->J, p->cmax, p->amax, p->d_slack, p->stream));
-    slack = p->d_slack;
-  }
-  CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out, slack), p->ctas, p->smem, p->stream));
+  CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out), p->ctas, p->smem, p->stream));
   return DL_OK;
 }
 
@@ -234,10 +228,9 @@ StepArgs step_args(dl_problem* p) {
   s.mu = p->d_mu;
   s.st = p->d_st;
   s.hist = p->d_hist;
-  s.m = p->M;
-  s.cmax = p->cmax;
-  for (int f = 0; f < 4; ++f) s.amax[f] = p->amax[f];
-  s.slack = p->d_slack + 1;
+  s.part = p->d_step_part;
+  s.done = p->d_step_done;
+  s.scal = p->d_step_scal;
   return s;
 }
 
@@ -359,7 +352,7 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
       (s = dev_alloc(p, &p->d_orig_off, nb)) || (s = dev_alloc(p, &p->d_acc, MJ + 4)) ||
       (s = dev_alloc(p, &p->d_ctr, 8)) || (s = dev_alloc(p, &p->d_D, MJ)) || (s = dev_alloc(p, &p->d_Dones, MJ)) ||
       (s = dev_alloc(p, &p->d_lam_in, MJ)) || (s = dev_alloc(p, &p->d_grad_out, MJ)) ||
-      (s = dev_alloc(p, &p->d_obj_out, 4)) || (s = dev_alloc(p, &p->d_slack, 2)))
+      (s = dev_alloc(p, &p->d_obj_out, 4)))
     return fail(s);
   if (d->v && ((s = dev_alloc(p, &p->d_vsq, nb)) || (s = dev_alloc(p, &p->d_vinv, nb)))) return fail(s);
   if (p->kind != DL_PROJ_BOXCUT) {  // queue for simplex blocks deferred by the fused kernel
@@ -441,19 +434,6 @@ dl_status dl_problem_create(const dl_problem_desc* d, dl_problem** out) {
   }
   CUDA_TRY(launch_jacobi_diag(nullptr, p->d_D, (int32_t)MJ, p->stream));
   CUDA_TRY(launch_jacobi_diag(nullptr, p->d_Dones, (int32_t)MJ, p->stream));
-  // magnitude bounds for the fp32 candidate filter: max|c|, max|a_f|
-  {
-    float* d_mx = nullptr;
-    if ((s = dev_alloc(p, &d_mx, 5))) return fail(s);
-    CUDA_TRY(launch_absmax(p->d_c, p->nnz_layout, d_mx, p->stream));
-    for (int f = 0; f < p->M; ++f)
-      CUDA_TRY(launch_absmax(p->d_a + (size_t)f * p->a_stride, p->nnz_layout, d_mx + 1 + f, p->stream));
-    float mx[5] = {0, 0, 0, 0, 0};
-    CUDA_TRY(cudaMemcpyAsync(mx, d_mx, 5 * sizeof(float), cudaMemcpyDeviceToHost, p->stream));
-    CUDA_TRY(cudaStreamSynchronize(p->stream));
-    p->cmax = mx[0];
-    for (int f = 0; f < p->M; ++f) p->amax[f] = mx[1 + f];
-  }
   CUDA_TRY(cudaStreamSynchronize(p->stream));
   // temporary plan arrays are not needed any more
   for (void* q : {(void*)d_perm, (void*)d_boff}) {
@@ -611,8 +591,11 @@ dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm) {
     dl_status s;
     if ((s = dev_alloc(p, &p->d_lam1, n)) || (s = dev_alloc(p, &p->d_lam2, n)) ||
         (s = dev_alloc(p, &p->d_lam2_prev, n)) || (s = dev_alloc(p, &p->d_G_prev, n)) ||
-        (s = dev_alloc(p, &p->d_mu, n)) || (s = dev_alloc(p, &p->d_st, 1)))
+        (s = dev_alloc(p, &p->d_mu, n)) || (s = dev_alloc(p, &p->d_st, 1)) ||
+        (s = dev_alloc(p, &p->d_step_part, 5 * kStepCtas)) || (s = dev_alloc(p, &p->d_step_done, 1)) ||
+        (s = dev_alloc(p, &p->d_step_scal, 2)))
       return s;
+    CUDA_TRY(cudaMemsetAsync(p->d_step_done, 0, sizeof(int32_t), p->stream));
   }
   // the captured solve graph bakes in the history buffer and the Jacobi diagonal: rebuild it
   if (p->graph) {
@@ -653,7 +636,6 @@ dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm) {
   for (double* q : {p->d_lam1, p->d_lam2, p->d_lam2_prev, p->d_G_prev})
     CUDA_TRY(cudaMemsetAsync(q, 0, n * sizeof(double), p->stream));
   CUDA_TRY(cudaMemsetAsync(p->d_mu, 0, n * sizeof(float), p->stream));
-  CUDA_TRY(launch_slack(p->d_mu, p->M, p->J, p->cmax, p->amax, p->d_slack + 1, p->stream));
   CUDA_TRY(cudaMemsetAsync(p->d_acc, 0, (n + 4) * sizeof(double), p->stream));
   CUDA_TRY(cudaMemsetAsync(p->d_ctr, 0, 8 * sizeof(int32_t), p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));  // st is a stack object

@@ -1075,7 +1075,7 @@ cudaError_t launch_t(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
   auto dk = deferred_kernel<M, WX>;
   e = cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
   if (e != cudaSuccess) return e;
-  dk<<<ctas, 256, dsmem, s>>>(a);
+  dk<<<4 * ctas, 256, dsmem, s>>>(a);  // 32 warps per SM: a storm of deferred blocks (large gamma) drains fast
   return cudaGetLastError();
 }
 

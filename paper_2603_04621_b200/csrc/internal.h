@@ -92,7 +92,6 @@ struct GradArgs {
   int32_t J, m;
   const double* gamma_ptr; // device gamma (solver) or nullptr -> gamma_val
   double gamma_val;
-  const float* slack;      // device: 2^-19 (m+1) (max|c| + sum_f max|a_f| max|lambda_f|)
   double r, u;             // polytope caps (inf where absent)
   int32_t kind;
   int32_t tile_cap;
@@ -110,6 +109,8 @@ cudaError_t launch_fused_grad(const GradArgs& a, int ctas, size_t smem, cudaStre
 template <int M>
 cudaError_t launch_fused_grad_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
 
+constexpr int kStepCtas = 64;  // CTAs of the AGD reduce kernel (partials buffer 5 x kStepCtas)
+
 struct StepArgs {
   int32_t n;               // m*J
   const double* D;         // Jacobi diagonal
@@ -120,9 +121,9 @@ struct StepArgs {
   float* mu;
   AgdDev* st;
   dl_iter_record* hist;
-  int32_t m;               // families (slack: per-family max |mu|)
-  float cmax, amax[4];     // max |c|, max |a_f| of the problem
-  float* slack;            // written for the next evaluation
+  double* part;            // [5 * kStepCtas] per-CTA partial sums
+  int32_t* done;           // CTA completion counter (0 between steps)
+  double* scal;            // [2] eta, beta of the step
 };
 cudaError_t launch_agd_step(const StepArgs& a, cudaStream_t s);
 
@@ -141,11 +142,6 @@ cudaError_t launch_row_sqnorms(const int32_t* dest, const float* a, int64_t a_st
                                int32_t J, double* out, cudaStream_t s);
 cudaError_t launch_jacobi_diag(const double* rowsq, double* D, int32_t n, cudaStream_t s);
 cudaError_t launch_fill_f64(double* p, double v, int64_t n, cudaStream_t s);
-// max |x| of a float array into *out (out zeroed by the call)
-cudaError_t launch_absmax(const float* x, int64_t n, float* out, cudaStream_t s);
-// slack = 2^-19 (m+1) (cmax + sum_f amax_f max_j |lam_f j|) for a dual point lam [m*J]
-cudaError_t launch_slack(const float* lam, int32_t m, int32_t J, float cmax, const float* amax4, float* out,
-                         cudaStream_t s);
 cudaError_t launch_scale_out(const double* D, const double* lam, double* out, int32_t n, cudaStream_t s);
 
 struct LayoutArgs {

@@ -2,6 +2,7 @@
 // Jacobi row norms (K4), layout build (K5).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 #include <cmath>
 
@@ -11,6 +12,7 @@ namespace dl {
 namespace {
 
 constexpr int kStepThreads = 1024;
+constexpr int kRedThreads = 256;
 
 // Deterministic block reduction of NV doubles (fixed tree over a fixed thread map).
 template <int NV>
@@ -33,33 +35,6 @@ __device__ void block_sum(double (&v)[NV], double (*sm)[32]) {
   __syncthreads();
 }
 
-template <int NV>
-__device__ void block_max(float (&v)[NV], float (*sm)[32]) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-    for (int o = 16; o > 0; o >>= 1) v[i] = fmaxf(v[i], __shfl_xor_sync(0xffffffffu, v[i], o));
-  if (lane == 0)
-#pragma unroll
-    for (int i = 0; i < NV; ++i) sm[i][warp] = v[i];
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    float t = 0.f;
-    for (int w = 0; w < nw; ++w) t = fmaxf(t, sm[i][w]);
-    v[i] = t;
-  }
-  __syncthreads();
-}
-
-// fl32 error bound of the fused kernel's s = fl(c + sum a lambda): 2^-19 (m+1) magnitude bound
-__device__ __forceinline__ float slack_of(int m, float cmax, const float* amax, const float* lmax) {
-  float B = cmax;
-  for (int f = 0; f < m; ++f) B += amax[f] * lmax[f];
-  return 1.9073486e-6f * (float)(m + 1) * B * 1.0001f;
-}
-
 __device__ __forceinline__ double gamma_at(const AgdDev& st, int64_t t) {
   if (!st.continuation) return st.gamma0;
   int64_t h = t / st.halve_every;
@@ -68,17 +43,22 @@ __device__ __forceinline__ double gamma_at(const AgdDev& st, int64_t t) {
 }
 
 // One AGD iteration (R5-R8; oracle/agd.py steps 2-5) from the accumulated
-// A x*(mu_t) (+ objective scalars).  Single CTA => every rank computes identical bits.
-__global__ void __launch_bounds__(kStepThreads) agd_step_kernel(const StepArgs a) {
-  __shared__ double sm[6][32];
-  __shared__ double s_eta, s_beta;
+// A x*(mu_t) (+ objective scalars), as two grid-wide kernels:
+//  agd_reduce_kernel: CTA c reduces rows [c chunk, (c+1) chunk) to 5 partial sums (fixed
+//   tree); the last CTA to finish adds the partials in CTA order, so the result does not
+//   depend on scheduling and every rank computes identical bits; it then sets eta, beta,
+//   the next gamma and the history record.
+//  agd_update_kernel: lambda update (eta, beta from the reduce) and accumulator reset.
+__global__ void __launch_bounds__(kRedThreads) agd_reduce_kernel(const StepArgs a) {
+  __shared__ double sm[5][32];
+  __shared__ bool last;
   const int n = a.n;
   const AgdDev st = *a.st;
   const int64_t t = st.t;
-  const double gamma = st.gamma;
-  // pass 1: dual value and norms
+  const int chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   double v[5] = {0, 0, 0, 0, 0};  // mu.grad, ||G||^2, ||grad_+||^2, ||G-Gp||^2, ||l2-l2p||^2
-  for (int r = threadIdx.x; r < n; r += kStepThreads) {
+  for (int r = r0 + threadIdx.x; r < r1; r += kRedThreads) {
     const double grad = a.acc[r] - (double)a.b[r];
     const double G = a.D[r] * grad;
     v[0] += (double)a.mu[r] * grad;
@@ -92,8 +72,23 @@ __global__ void __launch_bounds__(kStepThreads) agd_step_kernel(const StepArgs a
     }
   }
   block_sum<5>(v, sm);
+  if (threadIdx.x < 5) a.part[threadIdx.x * gridDim.x + blockIdx.x] = v[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.done, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 5) {  // fixed order over the CTAs
+    double q = 0.0;
+    for (int c = 0; c < (int)gridDim.x; ++c) q += __ldcg(a.part + threadIdx.x * gridDim.x + c);
+    sm[threadIdx.x][0] = q;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    const double g = a.acc[n] + a.acc[n + 1] + v[0];
+    *a.done = 0;
+    const double gamma = st.gamma;
+    const double g = a.acc[n] + a.acc[n + 1] + sm[0][0];
     const bool changed = t > 0 && gamma != st.gamma_prev;
     const double cap = st.max_step * gamma / st.gamma_ref;
     double eta;
@@ -102,20 +97,20 @@ __global__ void __launch_bounds__(kStepThreads) agd_step_kernel(const StepArgs a
     } else if (changed) {
       eta = fmin(st.eta * gamma / st.gamma_prev, cap);
     } else {
-      const double dl = sqrt(v[4]), dg = sqrt(v[3]);
+      const double dl = sqrt(sm[4][0]), dg = sqrt(sm[3][0]);
       eta = (dl > 0.0 && dg > 0.0) ? fmin(dl / dg, cap) : cap;
     }
     const int64_t k = changed ? 1 : st.k;
-    s_eta = eta;
-    s_beta = (double)(k - 1) / (double)(k + 2);
+    a.scal[0] = eta;
+    a.scal[1] = (double)(k - 1) / (double)(k + 2);
     if (t < st.hist_cap) {
       dl_iter_record rec;
       rec.iter = t;
       rec.g = g;
       rec.gamma = gamma;
       rec.eta = eta;
-      rec.gnorm = sqrt(v[1]);
-      rec.infeas = sqrt(v[2]);
+      rec.gnorm = sqrt(sm[1][0]);
+      rec.infeas = sqrt(sm[2][0]);
       rec.nnz_x = a.acc[n + 2];
       a.hist[t] = rec;
     }
@@ -127,12 +122,13 @@ __global__ void __launch_bounds__(kStepThreads) agd_step_kernel(const StepArgs a
     nst.k = k + 1;
     *a.st = nst;
   }
-  __syncthreads();
-  const double eta = s_eta, beta = s_beta;
-  // pass 2: lam1' = max(lam2 + eta G, 0); lam2' = max(lam1' + beta (lam1' - lam1), 0)
-  float lmax[4] = {0.f, 0.f, 0.f, 0.f};
-  const int J = n / a.m;
-  for (int r = threadIdx.x; r < n; r += kStepThreads) {
+}
+
+// lam1' = max(lam2 + eta G, 0); lam2' = max(lam1' + beta (lam1' - lam1), 0); mu = fl32(D lam2')
+__global__ void __launch_bounds__(kRedThreads) agd_update_kernel(const StepArgs a) {
+  const int n = a.n;
+  const double eta = a.scal[0], beta = a.scal[1];
+  for (int r = blockIdx.x * kRedThreads + threadIdx.x; r < n; r += gridDim.x * kRedThreads) {
     const double grad = a.acc[r] - (double)a.b[r];
     const double G = a.D[r] * grad;
     const double l2 = a.lam2[r];
@@ -142,38 +138,13 @@ __global__ void __launch_bounds__(kStepThreads) agd_step_kernel(const StepArgs a
     a.lam2_prev[r] = l2;
     a.lam1[r] = l1n;
     a.lam2[r] = l2n;
-    const float mu = (float)(a.D[r] * l2n);
-    a.mu[r] = mu;
-    const int f = r / J;
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q == f) lmax[q] = fmaxf(lmax[q], fabsf(mu));
+    a.mu[r] = (float)(a.D[r] * l2n);
     a.acc[r] = 0.0;
   }
-  if (threadIdx.x < 4) a.acc[n + threadIdx.x] = 0.0;
-  if (threadIdx.x < 8) a.ctr[threadIdx.x] = 0;
-  __shared__ float smx[4][32];
-  block_max<4>(lmax, smx);
-  if (threadIdx.x == 0) *a.slack = slack_of(a.m, a.cmax, a.amax, lmax);
-}
-
-__global__ void __launch_bounds__(kStepThreads) slack_kernel(const float* lam, int32_t m, int32_t J, float cmax,
-                                                             float a0, float a1, float a2, float a3, float* out) {
-  __shared__ float smx[4][32];
-  float lmax[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int f = 0; f < m; ++f)
-    for (int j = threadIdx.x; j < J; j += kStepThreads) lmax[f] = fmaxf(lmax[f], fabsf(lam[(size_t)f * J + j]));
-  block_max<4>(lmax, smx);
-  const float amax[4] = {a0, a1, a2, a3};
-  if (threadIdx.x == 0) *out = slack_of(m, cmax, amax, lmax);
-}
-
-__global__ void absmax_kernel(const float* x, int64_t n, unsigned int* out) {
-  float v = 0.f;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    if (fabsf(x[i]) < __int_as_float(0x7f800000)) v = fmaxf(v, fabsf(x[i]));  // layout padding is +inf
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(v));  // v >= 0: uint order = float order
+  if (blockIdx.x == 0) {
+    if (threadIdx.x < 4) a.acc[n + threadIdx.x] = 0.0;
+    if (threadIdx.x < 8) a.ctr[threadIdx.x] = 0;
+  }
 }
 
 // grad = A x - b (or A x if partial); obj = {g, c^T x, reg, nnz(x)}.
@@ -250,19 +221,11 @@ __global__ void build_layout_kernel(const LayoutArgs a) {
 }  // namespace
 
 cudaError_t launch_agd_step(const StepArgs& a, cudaStream_t s) {
-  agd_step_kernel<<<1, kStepThreads, 0, s>>>(a);
-  return cudaGetLastError();
-}
-cudaError_t launch_absmax(const float* x, int64_t n, float* out, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(float), s);
-  if (e != cudaSuccess || n == 0) return e;
-  absmax_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(x, n,
-                                                                                 reinterpret_cast<unsigned int*>(out));
-  return cudaGetLastError();
-}
-cudaError_t launch_slack(const float* lam, int32_t m, int32_t J, float cmax, const float* amax4, float* out,
-                         cudaStream_t s) {
-  slack_kernel<<<1, kStepThreads, 0, s>>>(lam, m, J, cmax, amax4[0], amax4[1], amax4[2], amax4[3], out);
+  const int ctas = std::max(1, std::min(kStepCtas, (a.n + kRedThreads - 1) / kRedThreads));
+  agd_reduce_kernel<<<ctas, kRedThreads, 0, s>>>(a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  agd_update_kernel<<<std::max(1, std::min(4 * 148, (a.n + kRedThreads - 1) / kRedThreads)), kRedThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
