@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from synth.matching import CONFIGS, generate
 from paper_2603_04621_b200 import MatchingProblem
-iters = int(sys.argv[1]) if len(sys.argv) > 1 else 3000
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 2510
 inst = generate(CONFIGS["1M_x_10k"], threads=16)
 gp = MatchingProblem.from_instance(inst)
 gp.set_jacobi(gp.row_sqnorms())
