@@ -31,6 +31,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOAD = "1M_x_10k"           # BASELINE.json configs[1]: 1M x 10k, ~100 nnz/source, simplex, Jacobi, 1 B200
+# workload -> (BASELINE.json configs index, projection kind, r, u, description); kinds as in include/dualip.h
+WORKLOADS = {
+    "tiny": (0, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
+    "1M_x_10k": (1, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
+    "100M_x_100k": (2, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
+    "multifamily_boxcut": (3, 1, 3.0, 1.0, "box-cut (0 <= x <= 1, sum x <= 3), 2 families (capacity + budget)"),
+    "powerlaw": (4, 0, 1.0, 1.0, "simplex (sum x <= 1), power-law block lengths 1..10k"),
+}
 GAP_TOL = 1e-3
 BURN_ITERS = 2500                # solver iterations before the timed steps (~ the 1e-3 gap point)
 
@@ -41,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=WORKLOAD)
+    ap.add_argument("--config", default=WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle CPU baseline")
     return ap.parse_args()
@@ -59,7 +67,13 @@ def shard_config(name, world):
 
 
 # --------------------------------------------------------------------------- oracle arms
-def oracle_sample(cfg, target_s=15.0, max_sources=200_000):
+def oracle_problem(inst, name):
+    from oracle.dual import Problem
+    _, kind, r, u, _ = WORKLOADS[name]
+    return Problem.from_instance(inst, kind=kind, r=r, u=(np.inf if kind == 0 else u))
+
+
+def oracle_sample(cfg, name, target_s=15.0, max_sources=200_000):
     """Time oracle.dual_eval on growing prefixes of the workload (same law, same
     seeds) until ~target_s of CPU work; returns (nnz/s, description)."""
     import dataclasses
@@ -69,7 +83,7 @@ def oracle_sample(cfg, target_s=15.0, max_sources=200_000):
     while True:
         inst, load = generate_shard(cfg, 0, n_src, threads=4)
         inst.b = capacities(cfg, load * (cfg.num_sources / max(n_src, 1)))
-        P = Problem.from_instance(inst)
+        P = oracle_problem(inst, name)
         lam = np.full(P.num_families * P.num_dests, 0.0)
         t0 = time.process_time()
         w0 = time.perf_counter()
@@ -88,17 +102,29 @@ def oracle_sample(cfg, target_s=15.0, max_sources=200_000):
 
 
 def run_reference(args):
+    """The base contract's reference arm for this tier: the fp64 oracle as it stands, on the host
+    cores, each step one dual-gradient evaluation of a bounded prefix of the workload (same law,
+    same seeds), the prefix sized so that warm-up + steps take about two minutes."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from synth.matching import CONFIGS
-    from oracle.dual import Problem, dual_eval
-    from synth.matching import generate_shard, capacities
+    from oracle.dual import dual_eval
+    from synth.matching import CONFIGS, capacities, generate_shard
     cfg = CONFIGS[args.config]
-    n_src = 20_000
-    inst, load = generate_shard(cfg, 0, n_src, threads=4)
-    inst.b = capacities(cfg, load * (cfg.num_sources / n_src))
-    P = Problem.from_instance(inst)
+    budget_s = 120.0 / max(1, args.steps + args.warmup)
+
+    def prefix(n):
+        inst, load = generate_shard(cfg, 0, n, threads=4)
+        inst.b = capacities(cfg, load * (cfg.num_sources / n))
+        return oracle_problem(inst, args.config)
+    n_src = min(500, cfg.num_sources)
+    P = prefix(n_src)
+    lam = np.zeros(P.num_families * P.num_dests)
+    t0 = time.perf_counter()
+    dual_eval(P, lam, 0.01)
+    per_src = (time.perf_counter() - t0) / n_src
+    n_src = int(min(cfg.num_sources, 200_000, max(500, budget_s / max(per_src, 1e-9))))
+    P = prefix(n_src)
     lam = np.zeros(P.num_families * P.num_dests)
     for _ in range(args.warmup):
         dual_eval(P, lam, 0.01)
@@ -107,7 +133,8 @@ def run_reference(args):
         dual_eval(P, lam, 0.01)
     dt = time.perf_counter() - t0
     v = P.nnz * args.steps / dt
-    sample = f"oracle.dual.dual_eval on the first {n_src} sources ({P.nnz} nnz) of {args.config}"
+    sample = (f"oracle.dual.dual_eval (fp64 numpy, 1 thread) on the first {n_src} sources ({P.nnz} nnz) "
+              f"of {args.config}, lambda = 0, gamma = 0.01")
     print(json.dumps({
         "impl": "reference", "metric": "nnz/s per dual-gradient eval", "value": v, "unit": "nnz/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
@@ -194,7 +221,8 @@ def main():
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    gp = MatchingProblem.from_instance(inst, device=local, stream=stream)
+    cfg_idx, kind, proj_r, proj_u, proj_desc = WORKLOADS[args.config]
+    gp = MatchingProblem.from_instance(inst, kind=kind, r=proj_r, u=proj_u, device=local, stream=stream)
     if world > 1:
         gp.comm_init(rank, world)
     rowsq = gp.row_sqnorms()
@@ -333,17 +361,19 @@ def main():
         achieved = algo_bytes / (kern_avg / 1e3) / 1e9
         cpu = None
         if world == 1 and not args.no_cpu:
-            v, sample = oracle_sample(base)
+            v, sample = oracle_sample(base, args.config)
             cpu = {"value": v, "unit": "nnz/s", "cores": 1, "kind": "oracle", "sample": sample}
         out = {
             "metric": "nnz/s per dual-gradient eval", "value": value, "unit": "nnz/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 data, f64 scores/accum",
             "data": "synthetic",
-            "config": {"workload": f"{args.config} (BASELINE configs[1])", "num_sources_per_gpu": I,
+            "config": {"workload": f"{args.config} (BASELINE configs[{cfg_idx}])", "num_sources_per_gpu": I,
                        "num_dests": base.num_dests, "families": m, "nnz_total": int(nnz_total),
-                       "projection": "simplex (sum x <= 1)", "jacobi": True,
-                       "l2": "inputs (12 B/nnz, >1 GB per GPU) exceed the 126 MB L2; no flush needed",
+                       "projection": proj_desc, "jacobi": True,
+                       "l2": (f"inputs ({8 + 4 * m} B/nnz, {algo_bytes / 1e9:.2f} GB per GPU) exceed the 126 MB L2; "
+                              "no flush needed" if algo_bytes > 4 * 126e6 else
+                              f"inputs ({algo_bytes / 1e6:.0f} MB) are L2-resident: not a bench workload"),
                        "parallelism": f"dp{world} (sources sharded, lambda replicated, 1 NCCL all-reduce/step)",
                        "step": "fused dual-gradient pass + all-reduce + on-device AGD step",
                        "timed_from_iteration": BURN_ITERS + args.warmup},
