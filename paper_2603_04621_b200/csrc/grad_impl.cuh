@@ -489,23 +489,29 @@ __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t
   ff = tsum<G>(ff);
   const bool free64 = phi_free64 <= 1e30 && ff <= r;
   if (S.free && !free64) S.phi = phi_free;  // the fp32 test was too optimistic: Newton from phi_free
-  const float ph32 = S.phi;
-  double ph = free64 ? phi_free64 : (double)ph32;
+  // fp64 phase on the exact d: safeguarded Newton on the piecewise-linear F, started at the fp32
+  // result, with a bracket lo < phi* <= hi kept from fp64 evaluations (F(lo) < r < F(hi)); ends when
+  // F(phi) == r (a flat piece included) or the bracket/step is at fp64 resolution.  Membership is
+  // never decided in fp32 here (an fp32 partition can put phi a few ulps(d32) inside a neighbouring
+  // piece, PAPER.md:125-134 readings R1/R7).
+  // initial bracket: F(lo) = 0 below every d; F(hi) >= r (simplex: the minimum entry alone reaches
+  // r at d_min + r; box-cut: >= K = ceil(r/u) entries capped at d_(K) + u <= d_max + u)
+  const double marg = 1.0 + 1e-6 * (fabs((double)dmn) + fabs(refd) * ginv + fabs((double)hi0));
+  double lo = (double)dmn - marg;
+  double hi = (double)fmaxf(hi0, S.phi) + marg;
+  double ph = free64 ? phi_free64 : (double)S.phi;
   bool fin = !active || free64;
-  bool use32 = true;
-  for (int it = 0; it < 8 && __any_sync(kFull, !fin); ++it) {
+  for (int it = 0; it < 40 && __any_sync(kFull, !fin); ++it) {
     double sM = 0.0;
     float nM = 0.f, nC = 0.f;
 #pragma unroll
     for (int k = 0; k < E; ++k) {
       if (cm >> k & 1u) {
-        const double dd = use32 ? 0.0 : dexact(k);
-        const bool lt = use32 ? d[k] < ph32 : dd < ph;
-        const bool cp = use32 ? d[k] <= ph32 - uf : dd <= ph - u;
-        if (lt) {
-          if (!cp) {
+        const double dd = dexact(k);
+        if (dd < ph) {
+          if (dd > ph - u) {
             nM += 1.f;
-            sM += use32 ? dexact(k) : dd;
+            sM += dd;
           } else {
             nC += 1.f;
           }
@@ -515,14 +521,17 @@ __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t
     nM = tsum<G>(nM);
     nC = tsum<G>(nC);
     sM = tsum<G>(sM);
-    use32 = false;
     if (!fin) {
-      if (nM > 0.f) {
-        const double np = (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM;
-        fin = np == ph;
-        ph = np;
+      const double F = (nC > 0.f ? u * nC : 0.0) + (nM > 0.f ? ph * nM - sM : 0.0);
+      if (F == r) {
+        fin = true;
       } else {
-        fin = true;  // flat F: any phi of the piece is a root (x is 0 or u there)
+        if (F > r) hi = ph;
+        else lo = ph;
+        double np = nM > 0.f ? (r - (nC > 0.f ? u * nC : 0.0) + sM) / nM : __longlong_as_double(0x7ff8000000000000LL);
+        if (!(np > lo && np < hi)) np = 0.5 * (lo + hi);
+        if (np == ph || !(hi - lo > 4e-16 * fmax(fabs(hi), fabs(lo)))) fin = true;
+        ph = np;
       }
     }
   }

@@ -17,7 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 from oracle.dual import BOX, BOXCUT, SIMPLEX, Problem, apply_A, dual_eval, row_sqnorms  # noqa: E402
 from oracle.layout import tile_plan  # noqa: E402
 from paper_2603_04621_b200 import MatchingProblem  # noqa: E402
-from synth.matching import GenConfig, generate  # noqa: E402
+from synth.matching import GenConfig, Instance, generate  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 
@@ -161,4 +161,38 @@ def test_edge_cases():
     torch.cuda.synchronize()
     np.testing.assert_array_equal(grad.cpu().numpy(), -np.ones(4))
     assert obj.cpu().numpy()[0] == -2.0
+    gp.close()
+
+
+@pytest.mark.parametrize("kind,r,u", [(BOXCUT, 3.0, 1.0), (BOXCUT, 2.5, 0.5), (SIMPLEX, 1.0, 1.0)])
+def test_near_flat_pieces(kind, r, u):
+    """Blocks built so that the threshold equation F(phi) = sum clip(phi - d, 0, u) = r has a flat
+    piece (or a kink) narrower than fp32 resolves: d_(K+1) - d_(K) = u (1 + delta), delta in
+    [1e-7, 1e-3] (box-cut), resp. ties of the simplex threshold within 1e-7 relative.  The exact
+    partition must be found (regression: an fp32 partition accepted as flat left x ~ 4e-5 on an
+    entry the oracle sets to 0, sum x > r)."""
+    rng = np.random.default_rng(33)
+    I, L, gamma = 3000, 96, 0.01
+    K = int(np.ceil(r / u)) if kind == BOXCUT else 1
+    lens = np.full(I, L)
+    rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    J = 4000
+    dest = np.concatenate([np.sort(rng.choice(J, L, replace=False)) for _ in range(I)]).astype(np.int32)
+    base = rng.uniform(-8.0, -5.0, I)
+    delta = 10.0 ** rng.uniform(-7, -3, I)
+    c = np.empty(I * L)
+    for i in range(I):
+        off = np.sort(rng.uniform(0.0, 2.0, L))                      # the rest of the block, in s units
+        off[:K] = np.sort(rng.uniform(0.0, 0.5 * u * gamma, K))        # K entries close to the minimum
+        gap = (u if kind == BOXCUT else 0.0) * gamma * (1.0 + delta[i])
+        off[K] = off[K - 1] + gap                                      # the (K+1)-th just past the flat piece
+        off[K + 1:] = np.maximum(off[K + 1:], off[K] + 3 * gamma)
+        c[rp[i]:rp[i + 1]] = base[i] + off[rng.permutation(L)]
+    c = c.astype(np.float32)
+    a = np.ones((1, I * L), np.float32)
+    b = np.full(J, 10.0, np.float32)
+    inst = Instance(I, J, 1, rp, dest, a, c, b)
+    gp = MatchingProblem.from_instance(inst, kind=kind, r=r, u=u)
+    P = Problem.from_instance(inst, kind=kind, r=r, u=(np.inf if kind == SIMPLEX else u))
+    check_grad(gp, P, np.zeros(J, np.float32), gamma)
     gp.close()
