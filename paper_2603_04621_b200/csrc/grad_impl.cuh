@@ -557,6 +557,11 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
                            const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
+  // candidates per lane on the register path.  OWN (E <= 8 slots per lane, blocks < 32 entries): a
+  // lane's candidates are its own slots, no shared list, nothing is ever deferred; otherwise the
+  // group's candidates are compacted into a shared list, <= 4 per lane (more: deferred)
+  constexpr bool OWN = E <= 8;
+  constexpr int CAP = OWN ? E : 4;
   const GradArgs& p = C.p;
   const int cap = p.tile_cap;
   const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
@@ -700,7 +705,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     }
     if (!active) cm = 0;
     // ---- compaction: the group's candidates (tile entry indices) are packed into a per-warp
-    // shared list so that lane q of the group owns candidates q, q+G, q+2G, q+3G (<= 4 G).
+    // shared list so that lane q of the group owns candidates q, q+G, .. (<= CAP G).
     const int nc = __popc(cm);
     int incl = nc;
 #pragma unroll
@@ -710,11 +715,11 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     }
     int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
     if constexpr (GEN) {
-      if (!__all_sync(kFull, T <= 4 * G)) {
+      if (!__all_sync(kFull, T <= CAP * G)) {
         generic_round<M, LAMS, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
         continue;
       }
-    } else if (T > 4 * G) {  // defer this block to deferred_kernel (exact generic solve there)
+    } else if (T > CAP * G) {  // defer this block to deferred_kernel (exact generic solve there)
       if (q == 0) {
         const int slot = atomicAdd(p.ctr + 6, 1);
         if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, end - start};
@@ -723,29 +728,38 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       incl = 0;
       T = 0;
     }
-    {
+    if constexpr (!OWN) {
       uint32_t m = cm;
-      int o = gi * 4 * G + incl - nc;
+      int o = gi * CAP * G + incl - nc;
       while (m) {
         const int k = __ffs(m) - 1;
         m &= m - 1;
         cand_s[o++] = (uint16_t)(start + slot_entry<LG, false>(q, k));
       }
+      __syncwarp();
     }
-    __syncwarp();
-    const int pmax = (__reduce_max_sync(kFull, (unsigned)T) + G - 1) >> LG;  // warp-uniform
+    // candidate slots to visit (warp-uniform): own slots -> the largest per-lane count
+    const int pmax = OWN ? (int)__reduce_max_sync(kFull, (unsigned)nc)
+                         : (int)((__reduce_max_sync(kFull, (unsigned)T) + G - 1) >> LG);
     const double refd = (double)ref;
     const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
-    double d64[4];
-    int ei[4];
+    double d64[CAP];
+    int ei[CAP];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < CAP; ++c) {
       d64[c] = kInfD;
       ei[c] = -1;
       if (c < pmax) {
-        const int idx = q + c * G;
-        if (idx < T) {
-          const int ee = cand_s[gi * 4 * G + idx];
+        const int idx = OWN ? c : q + c * G;
+        if (idx < (OWN ? nc : T)) {
+          int ee;
+          if constexpr (OWN) {  // c-th candidate slot of the lane itself
+            uint32_t m = cm;
+            for (int z = 0; z < c; ++z) m &= m - 1;
+            ee = start + slot_entry<LG, false>(q, __ffs(m) - 1);
+          } else {
+            ee = cand_s[gi * CAP * G + idx];
+          }
           d64[c] = (score_smem(C, sd, sc, sa, cap, ee) - refd) * ginv;
           ei[c] = ee;
         }
@@ -761,7 +775,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     {
       double sl = 0.0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < CAP; ++c)
         if (c < pmax && ei[c] >= 0) sl += d64[c];
       const double sm = tsum<G>(sl);
       if (!done) phi = (r + sm) * (T <= kRcpN ? rcp_s[T] : 1.0 / T);
@@ -771,7 +785,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       int cnt = 0;
       double sl = 0.0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < CAP; ++c)
         if (c < pmax) {
           const bool in = d64[c] < phi;
           cnt += tcount<G>(in, gmask);
@@ -791,7 +805,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       const double ph = T == 1 ? phi_free : fmin(phi_free, phi);
       const double cap_x = T == 1 ? r : kInfD;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CAP; ++c) {
         if (c < pmax && ei[c] >= 0) {
           const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
           if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ei[c], x, vs, b, ei[c] - start);
@@ -1053,8 +1067,57 @@ __global__ void __launch_bounds__(256) deferred_kernel(const __grid_constant__ G
 #pragma unroll
     for (int k = 0; k < 8; ++k)
       if (s32[k] <= T) cm |= 1u << k;
-    // the block's entries sit at [0, len) of the warp's stage; orig_off / x_out use de.b
-    generic_round<M, false, WX, 5, 8, false>(C, sd, sc, sa, kStage, lane, 0, true, de.b, vs, ginv, cm, ref, s32);
+    // the block's entries sit at [0, len) of the warp's stage (slot k of the lane: entry lane + 32 k);
+    // orig_off / x_out use de.b.  Michelot in fp64 on the lane's own candidates (<= 8 per lane), as
+    // the fast path of small_tile, with warp-wide sums.
+    const double refd = (double)ref;
+    const double phi_free = -refd * ginv;
+    const int nc = __popc(cm);
+    const int nT = __reduce_add_sync(kFull, (unsigned)nc);
+    const int pmax = (int)__reduce_max_sync(kFull, (unsigned)nc);
+    double d64[8];
+    int ei[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      d64[c] = kInfD;
+      ei[c] = -1;
+      if (c < nc) {
+        uint32_t m = cm;
+        for (int z = 0; z < c; ++z) m &= m - 1;
+        const int e = lane + 32 * (__ffs(m) - 1);
+        d64[c] = (score_smem(C, sd, sc, sa, kStage, e) - refd) * ginv;
+        ei[c] = e;
+      }
+    }
+    double sl = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (ei[c] >= 0) sl += d64[c];
+    double phi = (p.r + tsum<32>(sl)) / (double)nT;
+    int cprev = nT;
+    for (int it = 0; it < 300 && nT > 1; ++it) {
+      int cnt = 0;
+      double s2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if (c < pmax) {
+          const bool in = d64[c] < phi;
+          cnt += __popc(__ballot_sync(kFull, in));
+          if (in) s2 += d64[c];
+        }
+      const double sm = tsum<32>(s2);
+      if (cnt == cprev || cnt == 0) break;
+      cprev = cnt;
+      phi = (p.r + sm) / (double)cnt;
+    }
+    const double ph = nT == 1 ? phi_free : fmin(phi_free, phi);
+    const double cap_x = nT == 1 ? p.r : kInfD;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (ei[c] >= 0) {
+        const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
+        if (x > 0.0) emit_smem(C, sd, sc, sa, kStage, ei[c], x, vs, de.b, ei[c]);
+      }
     __syncwarp();
   }
   double cx = C.cx, rg = C.reg;
