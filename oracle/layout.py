@@ -13,7 +13,9 @@ blocks out bucket-contiguously in HBM and cuts each bucket into *tiles*
 * blocks are ordered by (bucket descending, source id ascending);
 * a bucket t >= BIG_BUCKET (length >= 256) block is a tile of its own, worked
   by a multi-warp group; smaller buckets are packed greedily, in that order,
-  into tiles of at most ``tile_cap`` entries;
+  into tiles of at most ``tile_cap`` entries; a tile holding more than one
+  round (``round_blocks(t)`` blocks) is trimmed to whole rounds, the trimmed
+  blocks opening the next tile (no warp round runs with idle block groups);
 * every tile starts at an entry offset that is a multiple of 4 (16-byte TMA
   alignment); blocks inside a tile are contiguous.
 
@@ -50,6 +52,12 @@ def group_lanes(t: int) -> int:
     return 1 if t <= 3 else min(2 ** (t - 3), 512)
 
 
+def round_blocks(t: int) -> int:
+    """Blocks of bucket t < BIG_BUCKET one warp works at a time (a "round"): 32 / G with the
+    group widths G of the fused kernel (1 lane for t <= 3, 2, 4, 4, 8, 16 lanes for t = 4..8)."""
+    return 32 // {1: 1, 2: 1, 3: 1, 4: 2, 5: 4, 6: 4, 7: 8, 8: 16}[t]
+
+
 def tile_plan(lengths, tile_cap: int):
     """Returns (perm, blk_off, tiles, total) -- see module docstring.
 
@@ -67,16 +75,17 @@ def tile_plan(lengths, tile_cap: int):
         if t >= BIG_BUCKET:
             groups = [[i] for i in members]
         else:
-            cur, cur_n = [], 0
-            for i in members:
-                s = int(lengths[i])
-                if cur and cur_n + s > tile_cap:
-                    groups.append(cur)
-                    cur, cur_n = [], 0
-                cur.append(i)
-                cur_n += s
-            if cur:
-                groups.append(cur)
+            R = round_blocks(t)
+            q = 0
+            while q < len(members):
+                n, tot = 0, 0
+                while q + n < len(members) and (n == 0 or tot + int(lengths[members[q + n]]) <= tile_cap):
+                    tot += int(lengths[members[q + n]])
+                    n += 1
+                if n > R and q + n < len(members):   # trim to whole rounds (the bucket's last tile keeps all)
+                    n -= n % R
+                groups.append(members[q:q + n])
+                q += n
         for grp in groups:
             off = (off + ALIGN - 1) // ALIGN * ALIGN
             start, b0 = off, len(perm)
@@ -107,4 +116,5 @@ def shard_bounds(row_ptr, world: int):
     return out
 
 
-__all__ = ["BIG_BUCKET", "ALIGN", "bucket_of", "bucket_plan", "group_lanes", "tile_plan", "shard_bounds"]
+__all__ = ["BIG_BUCKET", "ALIGN", "bucket_of", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
+           "shard_bounds"]

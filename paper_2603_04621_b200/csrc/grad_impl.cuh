@@ -638,9 +638,15 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       continue;
     }
     const double r = p.r;
-    if (GEN && kind == DL_PROJ_BOXCUT) {
-      const float slack_m = M == 1 ? 0.f : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
-      // window above the K-th smallest s: active d < phi <= d_(K) + u, K = ceil(r/u)
+    // candidate window: entries that can be active.  Simplex: active d < phi <= r, i.e.
+    // s - s_min < gamma_i r; frame origin ref = s_min.  Box-cut: active d < phi <= d_(K) + u,
+    // K = ceil(r/u) (the K smallest at the cap already reach r); frame origin ref = s_(K).
+    // The slack covers the two roundings of s_j - ref and of the threshold sum: M = 1: 2^-21
+    // (|ref| + width) (>= 2.6x the bound 2^-24 (3 |ref| + 2 width)); M > 1: 2^-22 (M+1) max mag.
+    const bool boxcut = GEN && kind == DL_PROJ_BOXCUT;
+    const float slack_m = M == 1 ? 0.f : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
+    float ref;
+    if (boxcut) {
       const double u = p.u;
       const int K = (int)ceil(r / u);
       float sk = 0.f, cnt = 0.f;  // sk: K-th smallest s32 (or the largest, if fewer than K)
@@ -673,7 +679,6 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         }
       }
       if (sat) {
-        // slack as for the simplex with ref = s_(K) and the window gamma_i u
         const float gu = (float)(u * C.gamma * vs);
         const float slack = M == 1 ? 4.7683716e-7f * (fabsf(sk) + gu) : slack_m;
         const float T = sk + (gu * 1.000001f + slack);
@@ -685,19 +690,11 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         for (int k = 0; k < E; ++k)
           if (s32[k] < kInfF) cm |= 1u << k;
       }
-      if (!active) cm = 0;
-      if constexpr (GEN)
-        generic_round<M, LAMS, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm,
-                                                sat ? sk : 0.f, s32);
-      continue;
-    }
-    // simplex: active d < phi <= r  =>  s - s_min < gamma_i r.  The block slack covers the two
-    // roundings of s_j - s_min and of the threshold sum: M = 1: 2^-21 (|ref| + gamma_i r)
-    // (>= 2.6x the bound 2^-24 (3 |ref| + 2 gamma_i r)); M > 1: 2^-22 (M+1) max mag (2x margin).
-    const float ref = tmin<G>(lmin);
-    const float gr = (float)(r * C.gamma * vs);
-    const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
-    {
+      ref = sat ? sk : tmin<G>(lmin);
+    } else {
+      ref = tmin<G>(lmin);
+      const float gr = (float)(r * C.gamma * vs);
+      const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : slack_m;
       const float T = ref + (gr * 1.000001f + slack);
 #pragma unroll
       for (int k = 0; k < E; ++k)
@@ -764,6 +761,69 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
           ei[c] = ee;
         }
       }
+    }
+    if (boxcut) {
+      // box-cut, exact on the candidates in fp64: theta = 0 when F(phi_free) <= r (F(phi) = sum
+      // clip(phi - d, 0, u)); else the root of F(phi) = r by Newton on the current piece,
+      // phi = (r - u |C| + sum_M d)/|M| (M = {phi - u < d < phi}, C = {d <= phi - u}), safeguarded by
+      // a bracket F(lo) < r < F(hi) with bisection; starts from "every candidate in M".
+      const double u = p.u;
+      double ff = 0.0, sl = 0.0, dmn = kInfD, dmx = -kInfD;
+#pragma unroll
+      for (int c = 0; c < CAP; ++c)
+        if (c < pmax && ei[c] >= 0) {
+          ff += fmin(fmax(phi_free - d64[c], 0.0), u);
+          sl += d64[c];
+          dmn = fmin(dmn, d64[c]);
+          dmx = fmax(dmx, d64[c]);
+        }
+      ff = tsum<G>(ff);
+      sl = tsum<G>(sl);
+      dmn = tmin<G>(dmn);
+      dmx = tmax<G>(dmx);
+      // free only inside the window (beyond it, the K smallest are capped: F >= K u >= r)
+      const bool free = ff <= r && phi_free <= dmx + u;
+      double lo = dmn, hi = dmx + u;  // F(lo) = 0 < r <= u T <= F(hi)
+      double ph = free ? phi_free : fmin(fmax((r + sl) / (double)max(T, 1), lo), hi);
+      bool fin = !active || free || T == 0;
+      for (int it = 0; it < 64 && __any_sync(kFull, !fin); ++it) {
+        double sM = 0.0;
+        int nM = 0, nC = 0;
+#pragma unroll
+        for (int c = 0; c < CAP; ++c)
+          if (c < pmax) {
+            const bool lt = d64[c] < ph;
+            const bool cp = d64[c] <= ph - u;
+            nM += tcount<G>(lt && !cp, gmask);
+            nC += tcount<G>(lt && cp, gmask);
+            if (lt && !cp) sM += d64[c];
+          }
+        sM = tsum<G>(sM);
+        if (!fin) {
+          const double uC = nC > 0 ? u * nC : 0.0;
+          const double F = uC + (nM > 0 ? ph * nM - sM : 0.0);
+          if (F == r) {
+            fin = true;
+          } else {
+            if (F > r) hi = ph;
+            else lo = ph;
+            double np = nM > 0 ? (r - uC + sM) / nM : 0.5 * (lo + hi);
+            if (!(np > lo && np < hi)) np = 0.5 * (lo + hi);
+            if (np == ph || !(hi - lo > 4e-16 * fmax(fabs(hi), fabs(lo)))) fin = true;
+            ph = np;
+          }
+        }
+      }
+      if (active) {
+#pragma unroll
+        for (int c = 0; c < CAP; ++c)
+          if (c < pmax && ei[c] >= 0) {
+            const double x = fmin(fmax(ph - d64[c], 0.0), u);
+            if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ei[c], x, vs, b, ei[c] - start);
+          }
+      }
+      __syncwarp();
+      continue;
     }
     // Michelot in fp64 on the candidates for the root phi* of F(phi) = sum max(phi - d, 0) = r
     // (every active entry is a candidate and phi* <= r + slack/gamma_i, so F over the candidates

@@ -47,6 +47,11 @@ struct Plan {
 };
 
 inline int bucket_of(int64_t s) { return 64 - __builtin_clzll((unsigned long long)s); }
+// blocks of a small bucket one warp works per round: 32 / G, G the group width of the fused
+// kernel (small_dispatch: 1 lane for t <= 3, then 2, 4, 4, 8, 16 lanes for t = 4..8)
+inline int round_blocks(int bucket) {
+  return bucket <= 3 ? 32 : bucket == 4 ? 16 : bucket <= 6 ? 8 : bucket == 7 ? 4 : 2;
+}
 inline int big_phase_of(int bucket) {  // bucket >= 12 -> phase 0 (16 warps) ... 9 -> phase 3 (2 warps)
   return bucket >= 12 ? 0 : 12 - bucket;
 }

@@ -47,23 +47,34 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
     P.tiles.push_back(tl);
   };
   for (int t = 64; t >= 1; --t) {
-    int64_t end = start[t] + count[t];
-    bool big = t >= kBigBucket;
-    bool open = false;
-    for (; b < end;) {
-      int64_t i = P.perm[b];
-      int64_t s = row_ptr[i + 1] - row_ptr[i];
-      P.max_len = std::max<int32_t>(P.max_len, (int32_t)s);
-      if (!open || big || P.tiles.back().nnz + s > tile_cap) {
-        open_tile(t);
-        open = true;
+    const int64_t end = start[t] + count[t];
+    const bool big = t >= kBigBucket;
+    while (b < end) {
+      // longest run of whole blocks from b that fits tile_cap (one block per tile when big), trimmed
+      // to whole warp rounds (round_blocks(t) blocks) when it exceeds one round and blocks remain
+      int64_t n = 0, tot = 0;
+      while (b + n < end) {
+        const int64_t i = P.perm[b + n];
+        const int64_t s = row_ptr[i + 1] - row_ptr[i];
+        if (n > 0 && (big || tot + s > tile_cap)) break;
+        tot += s;
+        ++n;
       }
+      if (!big) {
+        const int64_t R = round_blocks(t);
+        if (n > R && b + n < end) n -= n % R;
+      }
+      open_tile(t);
       Tile& tl = P.tiles.back();
-      P.blk_off[b] = off;
-      off += s;
-      tl.nnz += (int32_t)s;
-      tl.nb += 1;
-      ++b;
+      for (int64_t q = 0; q < n; ++q, ++b) {
+        const int64_t i = P.perm[b];
+        const int64_t s = row_ptr[i + 1] - row_ptr[i];
+        P.max_len = std::max<int32_t>(P.max_len, (int32_t)s);
+        P.blk_off[b] = off;
+        off += s;
+        tl.nnz += (int32_t)s;
+        tl.nb += 1;
+      }
     }
   }
   P.total = off;

@@ -5,7 +5,8 @@ import math
 
 import numpy as np
 
-from oracle.layout import ALIGN, BIG_BUCKET, bucket_of, bucket_plan, group_lanes, shard_bounds, tile_plan
+from oracle.layout import (ALIGN, BIG_BUCKET, bucket_of, bucket_plan, group_lanes, round_blocks, shard_bounds,
+                           tile_plan)
 
 
 def test_bucket_bracket():
@@ -33,6 +34,15 @@ def test_launch_bound_and_padding_bound():
             assert launches <= 1 + math.floor(math.log2(lens.max()))
         for t, ids in plan.items():  # padded slab waste < 2x true entries
             assert len(ids) * (2 ** t - 1) < 2 * lens[ids].sum()
+
+
+def test_round_blocks_match_group_widths():
+    """round_blocks(t) = 32 / G(t): 32 one-lane groups for t <= 3, 16 two-lane groups for t = 4, ...,
+    2 sixteen-lane groups for t = 8 (E G >= 2^t slots hold every block of the bucket, E <= 16)."""
+    E = {1: 8, 2: 8, 3: 8, 4: 8, 5: 8, 6: 16, 7: 16, 8: 16}
+    for t in range(1, BIG_BUCKET):
+        G = 32 // round_blocks(t)
+        assert G * round_blocks(t) == 32 and E[t] * G >= 2 ** t
 
 
 def test_group_lanes_hold_block_in_8_per_lane():
@@ -71,10 +81,18 @@ def test_tile_plan_invariants():
             else:
                 assert tn <= cap
         assert covered == len(perm)
-        # greedy maximality: the next block of the same bucket did not fit
+        # greedy maximality, trimmed to whole warp rounds: a tile followed by one of the same bucket
+        # holds the longest run from its first block that fits tile_cap, cut down to a multiple of
+        # round_blocks(t) when the run exceeds one round
         for (a, b) in zip(tiles, tiles[1:]):
             if a[4] == b[4] and a[4] < BIG_BUCKET:
-                assert a[3] + lens[perm[b[0]]] > cap
+                run, tot = 0, 0
+                while a[0] + run < len(perm) and bucket_of(int(lens[perm[a[0] + run]])) == a[4] and \
+                        (run == 0 or tot + lens[perm[a[0] + run]] <= cap):
+                    tot += lens[perm[a[0] + run]]
+                    run += 1
+                R = round_blocks(a[4])
+                assert a[1] == (run if run <= R else run - run % R)
         assert total >= int(lens.sum())
 
 
