@@ -175,6 +175,7 @@ struct SmemHead {
   double red[2][kWarps][3];
   double rcp[kRcpN + 1];          // 1/n, n = 0..kRcpN (copied from c_rcp: divergent n, no constant-bank replays)
   int32_t slot[16];
+  int32_t ccount[16];             // candidate-list fill of each big-block group (phase 1)
 };
 static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
 
@@ -361,6 +362,137 @@ __device__ __forceinline__ T tmax(T v) {
 template <int G>
 __device__ __forceinline__ int tcount(bool pred, uint32_t gmask) {
   return __popc(__ballot_sync(kFull, pred) & gmask);
+}
+
+// Michelot in fp64 by one warp on up to 8 candidates per lane (d64[c] valid for c < own count):
+// phi* of F(phi) = sum max(phi - d, 0) = r over the candidates, threshold min(phi_free, phi*) (theta = 0
+// exactly when phi_free <= phi*); a single candidate gets x = min(phi_free, r).  emit(c, x) for x > 0.
+template <class EmitF>
+__device__ __forceinline__ void warp_michelot(const double (&d64)[8], int own, double r, double phi_free,
+                                              EmitF&& emit) {
+  const int nT = (int)__reduce_add_sync(kFull, (unsigned)own);
+  const int pmax = (int)__reduce_max_sync(kFull, (unsigned)own);
+  double sl = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < own) sl += d64[c];
+  double phi = (r + tsum<32>(sl)) / (double)max(nT, 1);
+  int cprev = nT;
+  for (int it = 0; it < 300 && nT > 1; ++it) {
+    int cnt = 0;
+    double s2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if (c < pmax) {
+        const bool in = c < own && d64[c] < phi;
+        cnt += __popc(__ballot_sync(kFull, in));
+        if (in) s2 += d64[c];
+      }
+    const double sm = tsum<32>(s2);
+    if (cnt == cprev || cnt == 0) break;
+    cprev = cnt;
+    phi = (r + sm) / (double)cnt;
+  }
+  const double ph = nT == 1 ? phi_free : fmin(phi_free, phi);
+  const double cap_x = nT == 1 ? r : kInfD;
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    if (c < own) {
+      const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
+      if (x > 0.0) emit(c, x);
+    }
+}
+
+// Big simplex block (>= 256 entries) by a multi-warp group, candidate version of big_block: pass 1
+// streams the block from global memory (coalesced) for the fp32 minimum; pass 2 re-streams it (L2)
+// and pushes the entries inside the candidate window (as small_tile) to a shared list; the group's
+// first warp then runs warp_michelot on the list (<= 256 candidates; more -> big_block, exact generic).
+template <int M, bool LAMS, bool WX>
+__device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, double* scr, int scr_cap,
+                                  double* scr_generic) {
+  const GradArgs& p = C.p;
+  const int len = tl.nnz;
+  const int64_t off = tl.off;
+  const int b = tl.b0;
+  const unsigned Jm1 = (unsigned)p.J - 1u;
+  int32_t* list = reinterpret_cast<int32_t*>(scr);
+  const int list_cap = min(256, 2 * scr_cap);
+  int32_t* cnt_s = &g.head->ccount[g.bar];
+  auto score32 = [&](int e, float& mg) {
+    const int j = (int)min((unsigned)__ldg(p.dest + off + e), Jm1);
+    const float cv = __ldg(p.c + off + e);
+    float sv = cv;
+    mg = fabsf(cv);
+#pragma unroll
+    for (int f = 0; f < M; ++f) {
+      const float av = __ldg(p.a + f * p.a_stride + off + e), lv = C.lam(f, j);
+      sv = fmaf(av, lv, sv);
+      if constexpr (M > 1) mg = fmaf(fabsf(av), fabsf(lv), mg);
+    }
+    return sv;
+  };
+  float lmin = kInfF, lmag = 0.f;
+  for (int e = g.gtid; e < len; e += g.G) {
+    float mg;
+    const float sv = score32(e, mg);
+    lmin = fminf(lmin, sv);
+    lmag = fmaxf(lmag, mg);
+  }
+  if (g.gtid == 0) *cnt_s = 0;  // ordered before pass 2 by the barrier of the reduce
+  double v[2] = {(double)lmin, -(double)lmag};
+  g.reduce(v, 1);
+  const float ref = (float)v[0];
+  const double vs = p.vsq ? (double)__ldg(p.vsq + b) : 1.0;
+  const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + b) : C.invgamma;
+  const float gr = (float)(p.r * C.gamma * vs);
+  const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * (float)(-v[1]);
+  const float T = ref + (gr * 1.000001f + slack);
+  const unsigned lt_mask = (1u << g.lane) - 1u;
+  for (int e0 = 0; e0 < len; e0 += g.G) {  // warp-uniform trip count
+    const int e = e0 + g.gtid;
+    float mg;
+    const bool cand = e < len && score32(min(e, len - 1), mg) <= T;
+    const unsigned m = __ballot_sync(kFull, cand);
+    int base = 0;
+    if (g.lane == 0 && m) base = atomicAdd(cnt_s, __popc(m));
+    base = __shfl_sync(kFull, base, 0);
+    if (cand) {
+      const int pos = base + __popc(m & lt_mask);
+      if (pos < list_cap) list[pos] = e;
+    }
+  }
+  g.sync();
+  const int nc = *cnt_s;
+  if (nc > list_cap) {  // candidate overflow: exact generic path
+    g.sync();
+    big_block<M, LAMS, WX>(C, g, tl, scr_generic);
+    return;
+  }
+  if (g.warp == g.warp0) {
+    const double refd = (double)ref;
+    double d64[8];
+    int ee[8];
+    int own = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      d64[c] = kInfD;
+      ee[c] = 0;
+      const int i = g.lane + 32 * c;
+      if (i < nc) {
+        ee[c] = list[i];
+        d64[c] = (score_global(C, off + ee[c]) - refd) * ginv;
+        own = c + 1;
+      }
+    }
+    warp_michelot(d64, own, p.r, -refd * ginv, [&](int c, double x) {
+      const int64_t e = off + ee[c];
+      float av[M];
+#pragma unroll
+      for (int f = 0; f < M; ++f) av[f] = __ldg(p.a + f * p.a_stride + e);
+      C.emit(__ldg(p.dest + e), __ldg(p.c + e), av, x, vs, b, ee[c]);
+    });
+  }
+  g.sync();  // the list and its counter are reused by the group's next block
 }
 
 // fp32 threshold solver state for the generic small path (partition only; the final
@@ -941,7 +1073,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (ti >= p.ph_begin[ph + 1]) break;
       const Tile tl = p.tiles[ti];
       double* scr = tl.nnz <= scr_cap ? scr_smem : p.gscratch + (size_t)blockIdx.x * p.gscratch_per_cta;
-      big_block<M, LAMS, WX>(C, g, tl, scr);
+      if (p.kind == DL_PROJ_SIMPLEX)
+        big_block_simplex<M, LAMS, WX>(C, g, tl, scr_smem, scr_cap, scr);
+      else
+        big_block<M, LAMS, WX>(C, g, tl, scr);
     }
   }
 
