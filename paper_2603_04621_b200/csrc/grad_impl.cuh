@@ -418,25 +418,45 @@ __device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& 
   int32_t* list = reinterpret_cast<int32_t*>(scr);
   const int list_cap = min(256, 2 * scr_cap);
   int32_t* cnt_s = &g.head->ccount[g.bar];
-  auto score32 = [&](int e, float& mg) {
-    const int j = (int)min((unsigned)__ldg(p.dest + off + e), Jm1);
-    const float cv = __ldg(p.c + off + e);
-    float sv = cv;
-    mg = fabsf(cv);
+  // U entries per thread per step, loads issued before use (the lambda gathers may miss to L2)
+  constexpr int U = 8;
+  auto scores = [&](int e0, float (&sv)[U], float (&mg)[U]) {
+    int j[U];
+    float cv[U], av[M][U];
 #pragma unroll
-    for (int f = 0; f < M; ++f) {
-      const float av = __ldg(p.a + f * p.a_stride + off + e), lv = C.lam(f, j);
-      sv = fmaf(av, lv, sv);
-      if constexpr (M > 1) mg = fmaf(fabsf(av), fabsf(lv), mg);
+    for (int u = 0; u < U; ++u) {
+      const int e = min(e0 + u * g.G, len - 1);
+      j[u] = (int)min((unsigned)__ldg(p.dest + off + e), Jm1);
+      cv[u] = __ldg(p.c + off + e);
+#pragma unroll
+      for (int f = 0; f < M; ++f) av[f][u] = __ldg(p.a + f * p.a_stride + off + e);
     }
-    return sv;
+    float lv[M][U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int f = 0; f < M; ++f) lv[f][u] = C.lam(f, j[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      sv[u] = cv[u];
+      mg[u] = fabsf(cv[u]);
+#pragma unroll
+      for (int f = 0; f < M; ++f) {
+        sv[u] = fmaf(av[f][u], lv[f][u], sv[u]);
+        if constexpr (M > 1) mg[u] = fmaf(fabsf(av[f][u]), fabsf(lv[f][u]), mg[u]);
+      }
+      if (e0 + u * g.G >= len) sv[u] = kInfF, mg[u] = 0.f;
+    }
   };
   float lmin = kInfF, lmag = 0.f;
-  for (int e = g.gtid; e < len; e += g.G) {
-    float mg;
-    const float sv = score32(e, mg);
-    lmin = fminf(lmin, sv);
-    lmag = fmaxf(lmag, mg);
+  for (int e0 = g.gtid; e0 < len; e0 += U * g.G) {
+    float sv[U], mg[U];
+    scores(e0, sv, mg);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      lmin = fminf(lmin, sv[u]);
+      lmag = fmaxf(lmag, mg[u]);
+    }
   }
   if (g.gtid == 0) *cnt_s = 0;  // ordered before pass 2 by the barrier of the reduce
   double v[2] = {(double)lmin, -(double)lmag};
@@ -448,17 +468,23 @@ __device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& 
   const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * (float)(-v[1]);
   const float T = ref + (gr * 1.000001f + slack);
   const unsigned lt_mask = (1u << g.lane) - 1u;
-  for (int e0 = 0; e0 < len; e0 += g.G) {  // warp-uniform trip count
-    const int e = e0 + g.gtid;
-    float mg;
-    const bool cand = e < len && score32(min(e, len - 1), mg) <= T;
-    const unsigned m = __ballot_sync(kFull, cand);
-    int base = 0;
-    if (g.lane == 0 && m) base = atomicAdd(cnt_s, __popc(m));
-    base = __shfl_sync(kFull, base, 0);
-    if (cand) {
-      const int pos = base + __popc(m & lt_mask);
-      if (pos < list_cap) list[pos] = e;
+  for (int b0 = 0; b0 < len; b0 += U * g.G) {  // warp-uniform trip count
+    float sv[U], mg[U];
+    scores(b0 + g.gtid, sv, mg);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = b0 + g.gtid + u * g.G;
+      const bool cand = sv[u] <= T;  // +inf past the block
+      const unsigned m = __ballot_sync(kFull, cand);
+      if (m) {
+        int base = 0;
+        if (g.lane == 0) base = atomicAdd(cnt_s, __popc(m));
+        base = __shfl_sync(kFull, base, 0);
+        if (cand) {
+          const int pos = base + __popc(m & lt_mask);
+          if (pos < list_cap) list[pos] = e;
+        }
+      }
     }
   }
   g.sync();
