@@ -86,6 +86,9 @@ CONFIGS = {
                                     num_families=2, seed=4),
     "powerlaw": GenConfig(num_sources=330_000_000, num_dests=100_000, length_law="powerlaw",
                           powerlaw_alpha=2.0, max_len=10_000, seed=5),
+    # the paper's per-iteration timing table: 25M sources x 10k destinations,
+    # sparsity 0.001 (10 eligible destinations per source); context, not a BASELINE config
+    "paper_table_25M": GenConfig(num_sources=25_000_000, num_dests=10_000, nnz_per_source=10.0, seed=6),
 }
 
 
