@@ -900,6 +900,7 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
     const double phi_free = -refd * ginv;  // x_free = max(phi_free - d, 0) = max(-s/gamma_i, 0)
     double d64[CAP];
     int ei[CAP];
+    uint32_t mo = cm;  // OWN: the lane's remaining candidate slots, consumed in slot order
 #pragma unroll
     for (int c = 0; c < CAP; ++c) {
       d64[c] = kInfD;
@@ -909,9 +910,8 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
         if (idx < (OWN ? nc : T)) {
           int ee;
           if constexpr (OWN) {  // c-th candidate slot of the lane itself
-            uint32_t m = cm;
-            for (int z = 0; z < c; ++z) m &= m - 1;
-            ee = start + slot_entry<LG, false>(q, __ffs(m) - 1);
+            ee = start + slot_entry<LG, false>(q, __ffs(mo) - 1);
+            mo &= mo - 1;
           } else {
             ee = cand_s[gi * CAP * G + idx];
           }
@@ -1006,9 +1006,11 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       for (int c = 0; c < CAP; ++c)
         if (c < pmax) {
           const bool in = d64[c] < phi;
-          cnt += tcount<G>(in, gmask);
+          if constexpr (G <= 4) cnt += in;  // narrow groups: lane counts, one group sum below
+          else cnt += tcount<G>(in, gmask);
           if (in) sl += d64[c];
         }
+      if constexpr (G <= 4) cnt = tsum<G>(cnt);
       const double sm = tsum<G>(sl);
       if (!done) {
         if (cnt == cprev || cnt == 0) {
