@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define DL_ABI_VERSION 1
+#define DL_ABI_VERSION 2
 
 typedef enum {
   DL_OK = 0,
@@ -87,6 +87,12 @@ typedef struct {
   int32_t max_block_len, num_buckets;
   int32_t num_sms, ctas;  /* grid of the fused kernel                                  */
   int64_t device_bytes;   /* device memory owned by the problem                        */
+  int32_t has_comm;       /* 1 once dl_comm_init created an NCCL communicator (any world) */
+  int32_t comm_rank, comm_world;
+  int32_t relabeled;      /* 1 if destinations are relabeled by popularity (R15) */
+  int32_t lambda_hot;     /* destination labels [0, lambda_hot) whose duals sit in shared memory
+                             (= num_dests when all of lambda fits; 0 when none is cached)     */
+  int32_t pad_;
 } dl_problem_info;
 
 /* ---- version / errors ---------------------------------------------------- */
@@ -97,6 +103,11 @@ const char* dl_last_error(void);
 /* Copies the CSR into the bucket-permuted, tile-aligned layout of DESIGN.md
  * "HBM layout".  Synchronises the stream once (reads row_ptr to plan). */
 dl_status dl_problem_create(const dl_problem_desc* desc, dl_problem** out);
+/* Same, but row_ptr, dest, a, c, b and v are HOST pointers (any host memory).  The edge
+ * arrays are streamed to the device in source chunks straight into the layout, so the
+ * device never holds a second copy of the input (BASELINE configs[2]: 5e9 edges).
+ * Synchronous. */
+dl_status dl_problem_create_host(const dl_problem_desc* desc, dl_problem** out);
 dl_status dl_problem_destroy(dl_problem* p);
 dl_status dl_problem_get_info(const dl_problem* p, dl_problem_info* out);
 /* Copies the layout back to HOST buffers (synchronous):
@@ -108,6 +119,12 @@ dl_status dl_problem_layout(const dl_problem* p, int64_t* perm, int64_t* blk_off
 /* Copies the permuted DEVICE arrays back to HOST (synchronous, tests):
  * dest[nnz_layout], c[nnz_layout], a[m*nnz_layout]; NULL skips. */
 dl_status dl_problem_layout_data(const dl_problem* p, int32_t* dest, float* c, float* a);
+
+/* Destination labels (R15): lab[j] = label of destination j (a permutation of
+ * [0, J)).  Labels order destinations by edge count, descending (ties: j ascending), when
+ * lambda does not fit in shared memory, so that the duals of the most-gathered destinations
+ * are the ones cached on chip; identity otherwise.  HOST output [num_dests]. */
+dl_status dl_problem_dest_labels(const dl_problem* p, int32_t* lab);
 
 /* Host-only planners (no GPU needed; same code dl_problem_create uses).
  * dl_plan_tiles: call with NULL outputs to get the counts, then with buffers
@@ -169,14 +186,22 @@ dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm);
 /* Runs the fused pass at the state's point mu_t into the problem's accumulator
  * (local shard only: all-reduce `acc` across ranks before dl_dual_step). */
 dl_status dl_agd_eval(dl_problem* p);
-/* acc: device fp64 [m*J + 4] = {A x (m*J), c^T x, reg, nnz(x), 0}; count returned in n. */
+/* acc: device fp64 [m*J + 4] = {A x (m*J), c^T x, reg, nnz(x), 0}; count returned in n.
+ * The m*J part is indexed by destination LABEL (k*J + lab[j]); all-reduce it as is. */
 dl_status dl_agd_accumulator(dl_problem* p, double** acc, int64_t* n);
+/* The solver's accumulated gradient at the current point mu_t, after dl_agd_eval (and, when
+ * sharded, the all-reduce of the accumulator) and before dl_dual_step: grad [m*J] fp64 =
+ * A x*(mu_t) - b in ORIGINAL order, obj [4] = {g(mu_t), c^T x*, reg, nnz(x*)}; device pointers. */
+dl_status dl_agd_gradient(dl_problem* p, double* grad, double* obj);
 /* One AGD step (R5-R8) from the accumulated gradient; also zeroes the
  * accumulator for the next dl_agd_eval and appends one dl_iter_record. */
 dl_status dl_dual_step(dl_problem* p);
 /* `iters` iterations of eval -> [NCCL all-reduce if dl_comm_init] -> step, captured
  * in a CUDA graph.  Asynchronous; read results with dl_agd_history / dl_agd_dual. */
 dl_status dl_solve(dl_problem* p, int64_t iters);
+/* The dual point mu_t = fl32(D lam2_t) the next dl_agd_eval evaluates (ORIGINAL coordinates,
+ * float32 [m*J], device or host auto-detected; host copies are synchronous). */
+dl_status dl_agd_point(dl_problem* p, float* mu_out);
 /* Copies records [0, min(cap, t)) to HOST; *count = records available. Synchronous. */
 dl_status dl_agd_history(dl_problem* p, dl_iter_record* out, int64_t cap, int64_t* count);
 /* Current duals, device or host (auto-detected), fp64 [m*J] in ORIGINAL coordinates:
@@ -187,7 +212,11 @@ dl_status dl_agd_dual(dl_problem* p, double* lam1_out, double* lam2_out);
 /* NCCL is loaded at run time (dlopen "libnccl.so.2").  Rank 0 calls
  * dl_comm_unique_id (128 bytes, host), shares it (e.g. torch.distributed
  * broadcast), then every rank calls dl_comm_init.  dl_solve then all-reduces
- * the m*J+4 accumulator once per iteration. */
+ * the m*J+4 accumulator once per iteration.  world == 1 creates a real one-rank
+ * communicator (the same code path; the all-reduce is then the identity).
+ * dl_comm_init all-reduces the destination edge counts and relabels every rank's
+ * layout with the GLOBAL labels (so the accumulators agree across ranks); it resets the
+ * AGD state (call dl_agd_init afterwards).  Calling it again replaces the communicator. */
 dl_status dl_comm_unique_id(void* id128);
 dl_status dl_comm_init(dl_problem* p, int32_t rank, int32_t world, const void* id128);
 /* In-place sum all-reduce of a device fp64 buffer over the problem's communicator

@@ -10,7 +10,10 @@
   DESIGN.md readings R5-R8, written here step by step in that order:
 
     t = 0, 1, ...:   gamma_t = max(gamma0 * 2^-floor(t/period), gamma_min)
-      1  mu_t   = fl32(D * lam2)            point handed to the gradient oracle (R7)
+      1  mu_t   = D * lam2                  point handed to the gradient oracle (fp64, the
+                                            paper's AGD; ``mu_fp32=True`` is a test-harness option
+                                            that rounds it to float32 like a caller handing the
+                                            gradient fp32 duals -- never the default)
       2  G_t    = D * (A x*(mu_t) - b)      preconditioned gradient; g_t = g(mu_t)
       3  eta_t  = init_step                                          if t = 0
                 = min(eta_{t-1} * gamma_t/gamma_{t-1}, cap(gamma_t))  if gamma changed (R6)
@@ -40,6 +43,7 @@ class AgdConfig:
     max_step: float = 1e-3
     init_step: float = 1e-5
     jacobi: bool = True
+    mu_fp32: bool = False            # harness option only (see module docstring, step 1)
 
 
 def gamma_at(cfg: AgdConfig, t: int) -> float:
@@ -81,7 +85,9 @@ def agd(P: Problem, iters: int, cfg: AgdConfig = AgdConfig(), callback=None) -> 
         gamma = gamma_at(cfg, t)
         if gamma_prev is not None and gamma != gamma_prev:
             k = 1                                                     # R6: momentum restart
-        mu = (d * lam2).astype(np.float32).astype(np.float64)         # 1
+        mu = d * lam2                                                 # 1
+        if cfg.mu_fp32:
+            mu = mu.astype(np.float32).astype(np.float64)
         ev = dual_eval(P, mu, gamma)
         G = d * ev.grad                                               # 2
         if t == 0:                                                    # 3

@@ -97,6 +97,22 @@ def tile_plan(lengths, tile_cap: int):
     return perm, blk_off, tiles, off
 
 
+def dest_labels(dest, num_dests: int, relabel: bool):
+    """Destination labels of the layout (R15): when the duals do not all fit on chip,
+    destinations are ordered by edge count, descending, ties by index ascending, and label l is
+    the l-th of that order; otherwise the identity.  Returns lab[j]."""
+    if not relabel:
+        return list(range(num_dests))
+    counts = [0] * num_dests
+    for j in dest:
+        counts[int(j)] += 1
+    order = sorted(range(num_dests), key=lambda j: (-counts[j], j))
+    lab = [0] * num_dests
+    for l, j in enumerate(order):
+        lab[j] = l
+    return lab
+
+
 def shard_bounds(row_ptr, world: int):
     """[B_0=0, B_1, ..., B_W=I] with B_w = min{i : row_ptr[i] >= floor(w*nnz/W)}."""
     I = len(row_ptr) - 1
@@ -117,4 +133,4 @@ def shard_bounds(row_ptr, world: int):
 
 
 __all__ = ["BIG_BUCKET", "ALIGN", "bucket_of", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
-           "shard_bounds"]
+           "dest_labels", "shard_bounds"]

@@ -45,7 +45,9 @@ class dl_problem_info(C.Structure):
                 ("num_blocks", C.c_int64), ("num_tiles", C.c_int64), ("num_big_tiles", C.c_int64),
                 ("num_dests", C.c_int32), ("num_families", C.c_int32), ("tile_cap", C.c_int32),
                 ("lambda_in_smem", C.c_int32), ("max_block_len", C.c_int32), ("num_buckets", C.c_int32),
-                ("num_sms", C.c_int32), ("ctas", C.c_int32), ("device_bytes", C.c_int64)]
+                ("num_sms", C.c_int32), ("ctas", C.c_int32), ("device_bytes", C.c_int64),
+                ("has_comm", C.c_int32), ("comm_rank", C.c_int32), ("comm_world", C.c_int32),
+                ("relabeled", C.c_int32), ("lambda_hot", C.c_int32), ("pad_", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -70,6 +72,8 @@ _sig = {
     "dl_abi_version": (C.c_int, []),
     "dl_last_error": (C.c_char_p, []),
     "dl_problem_create": (C.c_int, [C.POINTER(dl_problem_desc), C.POINTER(C.c_void_p)]),
+    "dl_problem_create_host": (C.c_int, [C.POINTER(dl_problem_desc), C.POINTER(C.c_void_p)]),
+    "dl_problem_dest_labels": (C.c_int, [_P, _P]),
     "dl_problem_destroy": (C.c_int, [_P]),
     "dl_problem_get_info": (C.c_int, [_P, C.POINTER(dl_problem_info)]),
     "dl_problem_layout": (C.c_int, [_P, _P, _P, _P]),
@@ -85,8 +89,10 @@ _sig = {
     "dl_agd_init": (C.c_int, [_P, C.POINTER(dl_agd_params)]),
     "dl_agd_eval": (C.c_int, [_P]),
     "dl_agd_accumulator": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "dl_agd_gradient": (C.c_int, [_P, _P, _P]),
     "dl_dual_step": (C.c_int, [_P]),
     "dl_solve": (C.c_int, [_P, C.c_int64]),
+    "dl_agd_point": (C.c_int, [_P, _P]),
     "dl_agd_history": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
     "dl_agd_dual": (C.c_int, [_P, _P, _P]),
     "dl_comm_unique_id": (C.c_int, [_P]),
@@ -137,6 +143,18 @@ def dl_problem_create(desc: dl_problem_desc):
     h = C.c_void_p()
     _ck(_lib.dl_problem_create(C.byref(desc), C.byref(h)))
     return h
+
+
+def dl_problem_create_host(desc: dl_problem_desc):
+    h = C.c_void_p()
+    _ck(_lib.dl_problem_create_host(C.byref(desc), C.byref(h)))
+    return h
+
+
+def dl_problem_dest_labels(h, num_dests):
+    lab = np.zeros(num_dests, np.int32)
+    _ck(_lib.dl_problem_dest_labels(h, ptr(lab)))
+    return lab
 
 
 def dl_problem_destroy(h):
@@ -225,12 +243,20 @@ def dl_agd_accumulator(h):
     return p.value, n.value
 
 
+def dl_agd_gradient(h, grad, obj):
+    _ck(_lib.dl_agd_gradient(h, ptr(grad), ptr(obj)))
+
+
 def dl_dual_step(h):
     _ck(_lib.dl_dual_step(h))
 
 
 def dl_solve(h, iters):
     _ck(_lib.dl_solve(h, int(iters)))
+
+
+def dl_agd_point(h, mu_out):
+    _ck(_lib.dl_agd_point(h, ptr(mu_out)))
 
 
 def dl_agd_history(h, cap=None):

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libdualip.so")
-SOURCES = ["grad_m1.cu", "grad_m2.cu", "grad_m3.cu", "grad_m4.cu", "plan.cpp", "grad.cu", "step.cu", "api.cu"]
+SOURCES = [f"grad_m{m}_k{k}.cu" for m in (1, 2, 3, 4) for k in (0, 1, 2)] + ["plan.cpp", "grad.cu", "step.cu", "api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

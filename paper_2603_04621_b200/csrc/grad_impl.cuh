@@ -1,5 +1,6 @@
-// Fused dual-gradient pass (K1).  Included once per family count M by
-// grad_m1.cu .. grad_m4.cu (DL_GRAD_M); launch_fused_grad (grad.cu) dispatches on m.
+// Fused dual-gradient pass (K1).  Included once per family count M and
+// polytope kind by grad_m<M>_k<KIND>.cu (DL_GRAD_M, DL_GRAD_KIND); launch_fused_grad (grad.cu)
+// dispatches on (m, kind).
 //
 // One persistent CTA per SM (16 warps).  For every source block i:
 //   s_ij = c_ij + sum_k a_kij lambda_kj                 (reduced cost)
@@ -179,17 +180,23 @@ struct SmemHead {
 };
 static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
 
-template <int M, bool LAMS, bool WX>
+template <int M, int LM, bool WX>
 struct Ctx {
   const GradArgs& p;
-  const float* lam_s;  // shared lambda (LAMS)
+  const float* lam_s;  // duals staged in shared memory (LM != kLamGlobal)
   double gamma, invgamma;
   double cx = 0.0, reg = 0.0;
   float nx = 0.f;
   __device__ Ctx(const GradArgs& pp, const float* ls, double g) : p(pp), lam_s(ls), gamma(g), invgamma(1.0 / g) {}
 
+  // dual of family f at destination label j: shared memory (all, or the hot labels [0, H) of
+  // the popularity order, R15) or global memory (L2-resident m*J floats)
   __device__ __forceinline__ float lam(int f, int j) const {
-    if constexpr (LAMS) return lam_s[f * p.J + j];
+    if constexpr (LM == kLamSmem) return lam_s[f * p.J + j];
+    if constexpr (LM == kLamHot) {  // one generic load: shared window for hot labels, else global
+      const float* q = j < p.lam_hot ? lam_s + f * p.lam_hot + j : p.lam + (size_t)f * p.J + j;
+      return *q;
+    }
     return __ldg(p.lam + (size_t)f * p.J + j);
   }
   // contribution of one positive x (fp64) to A x, the objective scalars and x_out
@@ -237,8 +244,8 @@ struct BigGroup {
   }
 };
 
-template <int M, bool LAMS, bool WX>
-__device__ __forceinline__ double score_global(const Ctx<M, LAMS, WX>& C, int64_t e) {
+template <int M, int LM, bool WX>
+__device__ __forceinline__ double score_global(const Ctx<M, LM, WX>& C, int64_t e) {
   const GradArgs& p = C.p;
   const int j = __ldg(p.dest + e);
   double s = (double)__ldg(p.c + e);
@@ -247,8 +254,8 @@ __device__ __forceinline__ double score_global(const Ctx<M, LAMS, WX>& C, int64_
   return s;
 }
 
-template <int M, bool LAMS, bool WX>
-__device__ void big_block(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, double* scr) {
+template <int M, int LM, bool WX>
+__device__ void big_block(Ctx<M, LM, WX>& C, BigGroup& g, const Tile& tl, double* scr) {
   const GradArgs& p = C.p;
   const int len = tl.nnz;
   const int64_t off = tl.off;
@@ -320,8 +327,8 @@ __device__ void big_block(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, doub
 }
 
 // ---------------------------------------------------------------- phase 2: small tiles
-template <int M, bool LAMS, bool WX>
-__device__ __forceinline__ double score_smem(const Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+template <int M, int LM, bool WX>
+__device__ __forceinline__ double score_smem(const Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
                                              const float* sa, int cap, int ee) {
   const int j = sd[ee];
   double s = (double)sc[ee];
@@ -330,8 +337,8 @@ __device__ __forceinline__ double score_smem(const Ctx<M, LAMS, WX>& C, const in
   return s;
 }
 
-template <int M, bool LAMS, bool WX>
-__device__ __forceinline__ void emit_smem(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc, const float* sa,
+template <int M, int LM, bool WX>
+__device__ __forceinline__ void emit_smem(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc, const float* sa,
                                           int cap, int ee, double x, double vs, int b, int e) {
   float av[M];
 #pragma unroll
@@ -364,18 +371,18 @@ __device__ __forceinline__ int tcount(bool pred, uint32_t gmask) {
   return __popc(__ballot_sync(kFull, pred) & gmask);
 }
 
-// Michelot in fp64 by one warp on up to 8 candidates per lane (d64[c] valid for c < own count):
+// Michelot in fp64 by one warp on up to 8 candidates per lane (d64[c] valid where bit c of vm is set):
 // phi* of F(phi) = sum max(phi - d, 0) = r over the candidates, threshold min(phi_free, phi*) (theta = 0
 // exactly when phi_free <= phi*); a single candidate gets x = min(phi_free, r).  emit(c, x) for x > 0.
 template <class EmitF>
-__device__ __forceinline__ void warp_michelot(const double (&d64)[8], int own, double r, double phi_free,
+__device__ __forceinline__ void warp_michelot(const double (&d64)[8], uint32_t vm, double r, double phi_free,
                                               EmitF&& emit) {
-  const int nT = (int)__reduce_add_sync(kFull, (unsigned)own);
-  const int pmax = (int)__reduce_max_sync(kFull, (unsigned)own);
+  const int nT = (int)__reduce_add_sync(kFull, (unsigned)__popc(vm));
+  const int pmax = 32 - (int)__reduce_min_sync(kFull, (unsigned)__clz(vm));  // highest slot in use + 1
   double sl = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c)
-    if (c < own) sl += d64[c];
+    if (vm >> c & 1u) sl += d64[c];
   double phi = (r + tsum<32>(sl)) / (double)max(nT, 1);
   int cprev = nT;
   for (int it = 0; it < 300 && nT > 1; ++it) {
@@ -384,7 +391,7 @@ __device__ __forceinline__ void warp_michelot(const double (&d64)[8], int own, d
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       if (c < pmax) {
-        const bool in = c < own && d64[c] < phi;
+        const bool in = (vm >> c & 1u) && d64[c] < phi;
         cnt += __popc(__ballot_sync(kFull, in));
         if (in) s2 += d64[c];
       }
@@ -397,7 +404,7 @@ __device__ __forceinline__ void warp_michelot(const double (&d64)[8], int own, d
   const double cap_x = nT == 1 ? r : kInfD;
 #pragma unroll
   for (int c = 0; c < 8; ++c)
-    if (c < own) {
+    if (vm >> c & 1u) {
       const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
       if (x > 0.0) emit(c, x);
     }
@@ -407,8 +414,8 @@ __device__ __forceinline__ void warp_michelot(const double (&d64)[8], int own, d
 // streams the block from global memory (coalesced) for the fp32 minimum; pass 2 re-streams it (L2)
 // and pushes the entries inside the candidate window (as small_tile) to a shared list; the group's
 // first warp then runs warp_michelot on the list (<= 256 candidates; more -> big_block, exact generic).
-template <int M, bool LAMS, bool WX>
-__device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& tl, double* scr, int scr_cap,
+template <int M, int LM, bool WX>
+__device__ void big_block_simplex(Ctx<M, LM, WX>& C, BigGroup& g, const Tile& tl, double* scr, int scr_cap,
                                   double* scr_generic) {
   const GradArgs& p = C.p;
   const int len = tl.nnz;
@@ -491,14 +498,14 @@ __device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& 
   const int nc = *cnt_s;
   if (nc > list_cap) {  // candidate overflow: exact generic path
     g.sync();
-    big_block<M, LAMS, WX>(C, g, tl, scr_generic);
+    big_block<M, LM, WX>(C, g, tl, scr_generic);
     return;
   }
   if (g.warp == g.warp0) {
     const double refd = (double)ref;
     double d64[8];
     int ee[8];
-    int own = 0;
+    uint32_t vm = 0;
 #pragma unroll
     for (int c = 0; c < 8; ++c) {
       d64[c] = kInfD;
@@ -507,10 +514,10 @@ __device__ void big_block_simplex(Ctx<M, LAMS, WX>& C, BigGroup& g, const Tile& 
       if (i < nc) {
         ee[c] = list[i];
         d64[c] = (score_global(C, off + ee[c]) - refd) * ginv;
-        own = c + 1;
+        vm |= 1u << c;
       }
     }
-    warp_michelot(d64, own, p.r, -refd * ginv, [&](int c, double x) {
+    warp_michelot(d64, vm, p.r, -refd * ginv, [&](int c, double x) {
       const int64_t e = off + ee[c];
       float av[M];
 #pragma unroll
@@ -546,8 +553,8 @@ __device__ __forceinline__ int slot_entry(int q, int k) {
   return V4 ? 4 * (q + (k >> 2) * (1 << LG)) + (k & 3) : q + k * (1 << LG);
 }
 
-template <int M, bool LAMS, bool WX, int LG, int E, bool V4>
-__device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t* sd, const float* sc,
+template <int M, int LM, bool WX, int LG, int E, bool V4>
+__device__ __forceinline__ void generic_round(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
                                               const float* sa, int cap, int q, int start, bool active, int b,
                                               double vs, double ginv, uint32_t cm, float ref, float (&d)[E]) {
   constexpr int G = 1 << LG;
@@ -706,18 +713,18 @@ __device__ __forceinline__ void generic_round(Ctx<M, LAMS, WX>& C, const int32_t
   }
 }
 
-// Short blocks of one tile (buckets < kBigBucket), G = 2^LG lanes per block, NG = 32/G blocks
-// per round, E entries (slots) per lane (E G > every length of the bucket).
-// GEN: the kernel variant that solves box-cut and overflowing simplex groups inline (generic
-// path); otherwise overflowing simplex groups are deferred to deferred_kernel.
-template <int M, bool LAMS, bool WX, int LG, int E, bool GEN>
-__device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
+// Short blocks of one tile (buckets < kBigBucket) for the BOX and BOX-CUT polytopes, G = 2^LG
+// lanes per block, NG = 32/G blocks per round, E entries (slots) per lane (E G > every length of
+// the bucket).  Groups with more candidates than the register path holds take the generic exact
+// solve (generic_round).  (Simplex tiles: small_tile_simplex below.)
+template <int M, int LM, bool WX, int LG, int E, bool GEN>
+__device__ void small_tile(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
                            const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
   // candidates per lane on the register path.  OWN (E <= 8 slots per lane, blocks < 32 entries): a
-  // lane's candidates are its own slots, no shared list, nothing is ever deferred; otherwise the
-  // group's candidates are compacted into a shared list, <= 4 per lane (more: deferred)
+  // lane's candidates are its own slots, no shared list; otherwise the group's candidates are
+  // compacted into a shared list, <= 4 per lane (more: generic_round)
   constexpr bool OWN = E <= 8;
   constexpr int CAP = OWN ? E : 4;
   const GradArgs& p = C.p;
@@ -869,19 +876,9 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
       if (q >= o) incl += v;
     }
     int T = __shfl_sync(kFull, incl, G - 1, G);  // candidates of the group
-    if constexpr (GEN) {
-      if (!__all_sync(kFull, T <= CAP * G)) {
-        generic_round<M, LAMS, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
-        continue;
-      }
-    } else if (T > CAP * G) {  // defer this block to deferred_kernel (exact generic solve there)
-      if (q == 0) {
-        const int slot = atomicAdd(p.ctr + 6, 1);
-        if (slot < p.defer_cap) p.defer[slot] = DeferEntry{tl.off + start, b, end - start};
-      }
-      cm = 0;
-      incl = 0;
-      T = 0;
+    if (!__all_sync(kFull, T <= CAP * G)) {  // many candidates: exact generic solve of the round
+      generic_round<M, LM, WX, LG, E, false>(C, sd, sc, sa, cap, q, start, active, b, vs, ginv, cm, ref, s32);
+      continue;
     }
     if constexpr (!OWN) {
       uint32_t m = cm;
@@ -1036,22 +1033,262 @@ __device__ void small_tile(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stag
   }
 }
 
-template <int M, bool LAMS, bool WX, bool GEN>
-__device__ __forceinline__ void small_dispatch(Ctx<M, LAMS, WX>& C, const Tile& tl, const char* stage, int lane,
+// ---------------------------------------------------------------- phase 2: short simplex blocks
+// Candidate-parallel exact projection onto {x >= 0, sum x <= r} (Eq. 4-5).
+//
+// A warp works a tile of short blocks in rounds of NG = 32/G blocks, G = 2^LG lanes per block,
+// E slots per lane (slot k of lane q = block entry q + k G):
+//  1. fp32 pass: s32 = fl(c + sum_k a_k lambda_k) for every slot, group minimum ref;
+//  2. window: only entries with s - s_min < gamma_i r can be positive (x_j > 0 needs d_j < phi* <=
+//     r + d_min); the fp32 filter s32 <= ref + gamma_i r (1 + 1e-6) + slack keeps all of them
+//     (slack bounds the fp32 rounding, R7/R14);
+//  3. the round's candidates (tile offset, group slot) are appended to a per-warp list in shared
+//     memory, one record per group (block, ref, its run in the list);
+//  4. flush (list full, group slots used up, or end of tile): the list is solved 32 candidates at
+//     a time, ONE CANDIDATE PER LANE, in chunks that hold whole blocks: exact fp64 rescoring
+//     d = (c + sum a lambda - ref)/gamma_i, then the closed form of the simplex threshold
+//         phi* = min_k (r + sum of the k smallest d) / k
+//     (the classical sort-and-threshold rule theta = max_k (sum_{i<=k} y_(i) - r)/k in the d frame,
+//     minimised over tie-group ends: rank_j = #{d <= d_j}, S_j = sum{d <= d_j}), threshold
+//     min(phi_free, phi*), x_j = max(threshold - d_j, 0); x > 0 is scattered (red.global.add.f64).
+//  Blocks with more than 32 candidates (large gamma) are solved right after their round by the
+//  whole warp (fp64 Michelot over the block's window, <= 8 entries per lane).
+struct ListSmem {  // per-warp candidate list and group records (meta + 512, kMetaSimplex bytes)
+  uint16_t e[kListCap];      // tile-relative entry
+  uint8_t g[kListCap];       // group slot
+  float ref[kGSlots];        // frame origin (fp32 block minimum)
+  int32_t blk[kGSlots];      // block (layout order)
+  uint16_t start[kGSlots];   // tile-relative first entry of the block
+  uint16_t lo[kGSlots];      // first list index of the block's candidates
+  uint8_t cnt[kGSlots];      // candidates of the block (<= 32)
+};
+static_assert(sizeof(ListSmem) + 512 <= kMetaSimplex, "candidate list fits the simplex metadata");
+
+template <int M, int LM, bool WX>
+__device__ __forceinline__ float score32_smem(const Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
+                                              const float* sa, int cap, int ee) {
+  float sv = sc[ee];
+  const int j = sd[ee];
+#pragma unroll
+  for (int f = 0; f < M; ++f) sv = fmaf(sa[f * cap + ee], C.lam(f, j), sv);
+  return sv;
+}
+
+// The whole warp solves one short block [start, end) of the stage (<= 255 entries, > 32 candidates):
+// window filter as in the pass, exact fp64 d of the candidates, fp64 Michelot.
+template <int M, int LM, bool WX>
+__device__ __noinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
+                                                const float* sa, int cap, int start, int end, int b, float ref,
+                                                float thr, double vs, double ginv, int lane) {
+  double d64[8];
+  uint32_t vm = 0;
+  const double refd = (double)ref;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int e = start + lane + 32 * c;
+    const bool ok = e < end && score32_smem(C, sd, sc, sa, cap, e) <= thr;
+    d64[c] = ok ? (score_smem(C, sd, sc, sa, cap, e) - refd) * ginv : kInfD;
+    if (ok) vm |= 1u << c;
+  }
+  warp_michelot(d64, vm, C.p.r, -refd * ginv, [&](int c, double x) {
+    const int e = start + lane + 32 * c;
+    emit_smem(C, sd, sc, sa, cap, e, x, vs, b, e - start);
+  });
+}
+
+template <int M, int LM, bool WX, int LG, int E>
+__device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
+                                   const uint16_t* rel_s, ListSmem& L, const double* rcp_s) {
+  constexpr int G = 1 << LG;
+  constexpr int NG = 32 >> LG;
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;  // family f at sa + f*cap
+  const int gi = lane >> LG, q = lane & (G - 1);
+  const int nrounds = (tl.nb + NG - 1) / NG;
+  const double r = p.r;
+  int nlist = 0, ngs = 0;  // warp-uniform fill of the list and of the group slots
+  for (int rd = 0; rd <= nrounds; ++rd) {
+    const bool last = rd == nrounds;
+    // ---- pass + window of round rd (registers: s32 die once the mask is formed)
+    uint32_t cm = 0;
+    int nc = 0, tg = 0, start = 0, end = 0, b = 0;
+    bool active = false;
+    float ref = 0.f, thr = 0.f;
+    if (!last) {
+      const int bb = rd * NG + gi;
+      active = bb < tl.nb;
+      b = tl.b0 + bb;
+      if (active) {
+        if (tl.rel_off >= 0) {
+          start = rel_s[bb];
+          end = rel_s[bb + 1];
+        } else {
+          start = (int)__ldg(p.blk_rel + b);
+          end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
+        }
+      }
+      const double vs = (p.vsq && active) ? (double)__ldg(p.vsq + b) : 1.0;
+      float s32[E];
+      float lmin = kInfF, lmag = 0.f;
+      const int lim = (end - start) - q;
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        const int ee = start + q + k * G;
+        const bool in = k * G < lim;
+        const int j = in ? sd[ee] : 0;  // reads past the tile stay inside shared memory (tail pad)
+        float sv = in ? sc[ee] : kInfF, mg = fabsf(sv);
+#pragma unroll
+        for (int f = 0; f < M; ++f) {
+          const float a_ = in ? sa[f * cap + ee] : 0.f, lv = C.lam(f, j);
+          sv = fmaf(a_, lv, sv);
+          if constexpr (M > 1) mg = fmaf(fabsf(a_), fabsf(lv), mg);
+        }
+        s32[k] = sv;
+        lmin = fminf(lmin, sv);
+        if constexpr (M > 1) lmag = sv < kInfF ? fmaxf(lmag, mg) : lmag;
+      }
+      ref = tmin<G>(lmin);
+      const float gr = (float)(r * C.gamma * vs);
+      // fp32 rounding bound of s_j - ref and the threshold (as r01, K1 step 2)
+      const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
+      thr = ref + (gr * 1.000001f + slack);
+#pragma unroll
+      for (int k = 0; k < E; ++k)
+        if (s32[k] <= thr) cm |= 1u << k;
+      if (!active) cm = 0;
+      nc = __popc(cm);
+      tg = tsum<G>(nc);
+      if (tg > 32) cm = 0, nc = 0;  // solved by the whole warp after the round
+    }
+    // warp-wide exclusive prefix of the candidate counts (lane order = group order)
+    int incl = nc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    // ---- flush: solve the list (before this round's candidates are written)
+    if (last || nlist + total > kListCap || ngs + NG > kGSlots) {
+      __syncwarp();
+      for (int base = 0; base < nlist;) {
+        const int i = base + lane;
+        const bool valid = i < nlist;
+        const int g = valid ? L.g[i] : 0;
+        const int lo = L.lo[g], n = L.cnt[g];
+        const unsigned nf = __ballot_sync(kFull, valid && lo + n > base + 32);
+        const int endc = nf ? __shfl_sync(kFull, lo, __ffs(nf) - 1) : min(nlist, base + 32);
+        const bool act = i < endc;
+        const int b_g = L.blk[g];
+        const double vs = p.vsq ? (double)__ldg(p.vsq + b_g) : 1.0;
+        const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + b_g) : C.invgamma;
+        const double refd = (double)L.ref[g];
+        const int e = L.e[valid ? i : 0];
+        const double d = act ? (score_smem(C, sd, sc, sa, cap, e) - refd) * ginv : 0.0;
+        // rank and prefix sum of d inside the block's run of lanes [lo - base, lo - base + n)
+        const int sl = lo - base;
+        const int nmax = (int)__reduce_max_sync(kFull, act ? (unsigned)n : 0u);
+        int rank = 0;
+        double S = 0.0;
+        for (int o = 0; o < nmax; ++o) {
+          const int src = act ? sl + min(o, n - 1) : lane;
+          const double dd = __shfl_sync(kFull, d, src);
+          if (act && o < n && dd <= d) {
+            ++rank;
+            S += dd;
+          }
+        }
+        const double f = (r + S) * rcp_s[act ? rank : 1];
+        double phi = f;
+        for (int o = 0; o < nmax; ++o) {
+          const int src = act ? sl + min(o, n - 1) : lane;
+          phi = fmin(phi, __shfl_sync(kFull, f, src));
+        }
+        if (act) {
+          const double x = fmax(fmin(-refd * ginv, phi) - d, 0.0);
+          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, e, x, vs, b_g, e - L.start[g]);
+        }
+        base = endc;
+      }
+      nlist = 0;
+      ngs = 0;
+      __syncwarp();
+    }
+    if (last) break;
+    // ---- append this round's candidates and group records
+    {
+      int pos = nlist + incl - nc;
+      uint32_t m = cm;
+      while (m) {
+        const int k = __ffs(m) - 1;
+        m &= m - 1;
+        L.e[pos] = (uint16_t)(start + q + k * G);
+        L.g[pos] = (uint8_t)(ngs + gi);
+        ++pos;
+      }
+      if (q == 0) {
+        const int gs = ngs + gi;
+        L.ref[gs] = ref;
+        L.blk[gs] = b;
+        L.start[gs] = (uint16_t)start;
+        L.lo[gs] = (uint16_t)(nlist + incl - nc);
+        L.cnt[gs] = (uint8_t)(active && tg <= 32 ? tg : 0);
+      }
+      nlist += total;
+      ngs += NG;
+      __syncwarp();
+    }
+    // ---- blocks with > 32 candidates: the whole warp, one block at a time
+    unsigned big = __ballot_sync(kFull, q == 0 && active && tg > 32);
+    while (big) {
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const int s0 = __shfl_sync(kFull, start, src), s1 = __shfl_sync(kFull, end, src);
+      const int bk = __shfl_sync(kFull, b, src);
+      const float rf = __shfl_sync(kFull, ref, src), th = __shfl_sync(kFull, thr, src);
+      const double vs = p.vsq ? (double)__ldg(p.vsq + bk) : 1.0;
+      const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + bk) : C.invgamma;
+      warp_block_simplex<M, LM, WX>(C, sd, sc, sa, cap, s0, s1, bk, rf, th, vs, ginv, lane);
+    }
+  }
+}
+
+template <int M, int LM, bool WX>
+__device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
+                                                       int lane, const uint16_t* rel_s, ListSmem& L,
+                                                       const double* rcp_s) {
+  switch (tl.bucket) {  // (LG, E): E 2^LG >= every length of bucket t; round_blocks(t) = 32 / 2^LG
+    case 1: small_tile_simplex<M, LM, WX, 0, 1>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 2: small_tile_simplex<M, LM, WX, 0, 3>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 3: small_tile_simplex<M, LM, WX, 0, 7>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 4: small_tile_simplex<M, LM, WX, 1, 8>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 5: small_tile_simplex<M, LM, WX, 2, 8>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 6: small_tile_simplex<M, LM, WX, 2, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    case 7: small_tile_simplex<M, LM, WX, 3, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+    default: small_tile_simplex<M, LM, WX, 4, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+  }
+}
+
+template <int M, int LM, bool WX, bool GEN>
+__device__ __forceinline__ void small_dispatch(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
                                                const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
   switch (tl.bucket) {  // (LG, E): E 2^LG > every length of bucket t
     case 1:
     case 2:
-    case 3: small_tile<M, LAMS, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 4: small_tile<M, LAMS, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 5: small_tile<M, LAMS, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 6: small_tile<M, LAMS, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 7: small_tile<M, LAMS, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    default: small_tile<M, LAMS, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 3: small_tile<M, LM, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 4: small_tile<M, LM, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 5: small_tile<M, LM, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 6: small_tile<M, LM, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 7: small_tile<M, LM, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    default: small_tile<M, LM, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
   }
 }
 
-template <int M, bool LAMS, bool WX, bool GEN>
+// KIND: DL_PROJ_SIMPLEX / DL_PROJ_BOXCUT / DL_PROJ_BOX; LM: lambda placement (kLam*).
+template <int M, int LM, bool WX, int KIND>
 __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_constant__ GradArgs p) {
   extern __shared__ __align__(128) char smem[];
   SmemHead* head = reinterpret_cast<SmemHead*>(smem);
@@ -1059,11 +1296,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   char* after_head = smem + 2048;
   float* lam_s = nullptr;
   size_t lam_bytes = 0;
-  if constexpr (LAMS) {
+  if constexpr (LM != kLamGlobal) {  // stage all duals, or those of the hot labels [0, H) per family
+    const int H = LM == kLamSmem ? p.J : p.lam_hot;
     lam_s = reinterpret_cast<float*>(after_head);
-    lam_bytes = ((size_t)M * p.J * 4 + 127) / 128 * 128;
-    const int n = M * p.J;
-    for (int i = threadIdx.x; i < n; i += kThreads) lam_s[i] = __ldg(p.lam + i);
+    lam_bytes = ((size_t)M * H * 4 + 127) / 128 * 128;
+    for (int f = 0; f < M; ++f)
+      for (int i = threadIdx.x; i < H; i += kThreads) lam_s[f * H + i] = __ldg(p.lam + (size_t)f * p.J + i);
   }
   char* tilebuf = after_head + lam_bytes;
   const uint32_t stage_bytes = (uint32_t)p.tile_cap * (8u + 4u * M);
@@ -1076,7 +1314,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   __syncthreads();
 
   const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
-  Ctx<M, LAMS, WX> C(p, lam_s, gamma);
+  Ctx<M, LM, WX> C(p, lam_s, gamma);
 
   // ---- phase 1: big blocks, groups of 16 / 8 / 4 / 2 warps; barrier ids unique per group
   for (int ph = 0; ph < kNumBigPhases; ++ph) {
@@ -1101,10 +1339,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (ti >= p.ph_begin[ph + 1]) break;
       const Tile tl = p.tiles[ti];
       double* scr = tl.nnz <= scr_cap ? scr_smem : p.gscratch + (size_t)blockIdx.x * p.gscratch_per_cta;
-      if (p.kind == DL_PROJ_SIMPLEX)
-        big_block_simplex<M, LAMS, WX>(C, g, tl, scr_smem, scr_cap, scr);
+      if constexpr (KIND == DL_PROJ_SIMPLEX)
+        big_block_simplex<M, LM, WX>(C, g, tl, scr_smem, scr_cap, scr);
       else
-        big_block<M, LAMS, WX>(C, g, tl, scr);
+        big_block<M, LM, WX>(C, g, tl, scr);
     }
   }
 
@@ -1117,10 +1355,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     constexpr int kChunk = 4;
     const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
     char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
-    char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMetaBytes;
+    constexpr int kMeta = KIND == DL_PROJ_SIMPLEX ? kMetaSimplex : kMetaBox;
+    char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMeta;
     const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
     const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
-    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // [128] candidate list
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // box kinds: [128] candidate list
+    ListSmem& lsm = *reinterpret_cast<ListSmem*>(meta + 512);               // simplex: candidate list
     uint64_t* bars = head->mbar[warp];
     uint64_t* dbars = head->mbar_desc[warp];
     if (lane == 0) {
@@ -1194,8 +1434,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (nhave) issue_tile(tn, st ^ 1);
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
-      small_dispatch<M, LAMS, WX, GEN>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,
-                                       head->rcp);
+      if constexpr (KIND == DL_PROJ_SIMPLEX)
+        small_dispatch_simplex<M, LM, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, lsm,
+                                          head->rcp);
+      else
+        small_dispatch<M, LM, WX, true>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,
+                                        head->rcp);
       __syncwarp();
       if (same) {
         ++pos;
@@ -1231,168 +1475,32 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   }
 }
 
-// Deferred simplex blocks (groups whose candidates overflowed the register fast path): one
-// warp per block, staged from global memory into shared memory, generic exact solve.
-template <int M, bool WX>
-__global__ void __launch_bounds__(256) deferred_kernel(const __grid_constant__ GradArgs p) {
-  constexpr int kW = 8;
-  constexpr int kStage = 256;  // entries (blocks here are < 256 long)
-  extern __shared__ __align__(128) char dsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  char* stage = dsm + (size_t)warp * kStage * (8 + 4 * M);
-  int32_t* sd = reinterpret_cast<int32_t*>(stage);
-  float* sc = reinterpret_cast<float*>(stage) + kStage;
-  float* sa = sc + kStage;
-  const int n = min(p.ctr[6], p.defer_cap);
-  const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
-  GradArgs pl = p;
-  pl.tile_cap = kStage;
-  Ctx<M, false, WX> C(pl, nullptr, gamma);
-  const unsigned Jm1 = (unsigned)p.J - 1u;
-  for (int i = blockIdx.x * kW + warp; i < n; i += gridDim.x * kW) {
-    const DeferEntry de = p.defer[i];
-    for (int e = lane; e < kStage; e += 32) {
-      const bool v = e < de.len;
-      sd[e] = v ? __ldg(p.dest + de.off + e) : 0;
-      sc[e] = v ? __ldg(p.c + de.off + e) : 0.f;
-#pragma unroll
-      for (int f = 0; f < M; ++f) sa[f * kStage + e] = v ? __ldg(p.a + f * p.a_stride + de.off + e) : 0.f;
-    }
-    __syncwarp();
-    double vs = 1.0, ginv = C.invgamma;
-    if (p.vsq) {
-      vs = (double)__ldg(p.vsq + de.b);
-      ginv = C.invgamma * (double)__ldg(p.vinv + de.b);
-    }
-    float s32[8];
-    float lmin = kInfF, lmag = 0.f;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int e = lane + 32 * k;
-      const int j = (int)min((unsigned)sd[e], Jm1);
-      float sv = sc[e], mg = fabsf(sc[e]);
-#pragma unroll
-      for (int f = 0; f < M; ++f) {
-        const float av = sa[f * kStage + e], lv = C.lam(f, j);
-        sv = fmaf(av, lv, sv);
-        mg = fmaf(fabsf(av), fabsf(lv), mg);
-      }
-      s32[k] = e < de.len ? sv : kInfF;
-      lmin = fminf(lmin, s32[k]);
-      if (s32[k] < kInfF) lmag = fmaxf(lmag, mg);  // padding (c = +inf) excluded
-    }
-    // candidate slack as in small_tile
-    const float ref = tmin<32>(lmin);
-    const float gr = (float)(p.r * gamma * vs);
-    const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<32>(lmag);
-    const float T = ref + (gr * 1.000001f + slack);
-    uint32_t cm = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (s32[k] <= T) cm |= 1u << k;
-    // the block's entries sit at [0, len) of the warp's stage (slot k of the lane: entry lane + 32 k);
-    // orig_off / x_out use de.b.  Michelot in fp64 on the lane's own candidates (<= 8 per lane), as
-    // the fast path of small_tile, with warp-wide sums.
-    const double refd = (double)ref;
-    const double phi_free = -refd * ginv;
-    const int nc = __popc(cm);
-    const int nT = __reduce_add_sync(kFull, (unsigned)nc);
-    const int pmax = (int)__reduce_max_sync(kFull, (unsigned)nc);
-    double d64[8];
-    int ei[8];
-#pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      d64[c] = kInfD;
-      ei[c] = -1;
-      if (c < nc) {
-        uint32_t m = cm;
-        for (int z = 0; z < c; ++z) m &= m - 1;
-        const int e = lane + 32 * (__ffs(m) - 1);
-        d64[c] = (score_smem(C, sd, sc, sa, kStage, e) - refd) * ginv;
-        ei[c] = e;
-      }
-    }
-    double sl = 0.0;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (ei[c] >= 0) sl += d64[c];
-    double phi = (p.r + tsum<32>(sl)) / (double)nT;
-    int cprev = nT;
-    for (int it = 0; it < 300 && nT > 1; ++it) {
-      int cnt = 0;
-      double s2 = 0.0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if (c < pmax) {
-          const bool in = d64[c] < phi;
-          cnt += __popc(__ballot_sync(kFull, in));
-          if (in) s2 += d64[c];
-        }
-      const double sm = tsum<32>(s2);
-      if (cnt == cprev || cnt == 0) break;
-      cprev = cnt;
-      phi = (p.r + sm) / (double)cnt;
-    }
-    const double ph = nT == 1 ? phi_free : fmin(phi_free, phi);
-    const double cap_x = nT == 1 ? p.r : kInfD;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if (ei[c] >= 0) {
-        const double x = fmin(fmax(ph - d64[c], 0.0), cap_x);
-        if (x > 0.0) emit_smem(C, sd, sc, sa, kStage, ei[c], x, vs, de.b, ei[c]);
-      }
-    __syncwarp();
-  }
-  double cx = C.cx, rg = C.reg;
-  float nx = C.nx;
-  for (int o = 16; o > 0; o >>= 1) {
-    cx += __shfl_xor_sync(kFull, cx, o);
-    rg += __shfl_xor_sync(kFull, rg, o);
-    nx += __shfl_xor_sync(kFull, nx, o);
-  }
-  if (lane == 0 && nx > 0.f) {
-    const size_t nn = (size_t)M * p.J;
-    atomicAdd(p.acc + nn + 0, cx);
-    atomicAdd(p.acc + nn + 1, rg);
-    atomicAdd(p.acc + nn + 2, (double)nx);
-  }
-}
-
-template <int M, bool LAMS, bool WX, bool GEN>
+template <int M, int LM, bool WX, int KIND>
 cudaError_t launch_t(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  auto k = fused_grad_kernel<M, LAMS, WX, GEN>;
+  auto k = fused_grad_kernel<M, LM, WX, KIND>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<ctas, kThreads, smem, s>>>(a);
-  e = cudaGetLastError();
-  if (e != cudaSuccess || GEN || !a.defer) return e;
-  const size_t dsmem = (size_t)8 * 256 * (8 + 4 * M);
-  auto dk = deferred_kernel<M, WX>;
-  e = cudaFuncSetAttribute(dk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsmem);
-  if (e != cudaSuccess) return e;
-  dk<<<4 * ctas, 256, dsmem, s>>>(a);  // 32 warps per SM: a storm of deferred blocks (large gamma) drains fast
   return cudaGetLastError();
 }
 
-template <int M>
-cudaError_t launch_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+template <int M, int KIND>
+cudaError_t launch_k(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
   const bool wx = a.x_out != nullptr;
-  if (a.kind == DL_PROJ_BOXCUT) {
-    if (a.lam_smem)
-      return wx ? launch_t<M, true, true, true>(a, ctas, smem, s) : launch_t<M, true, false, true>(a, ctas, smem, s);
-    return wx ? launch_t<M, false, true, true>(a, ctas, smem, s) : launch_t<M, false, false, true>(a, ctas, smem, s);
-  }
-  if (a.lam_smem)
-    return wx ? launch_t<M, true, true, false>(a, ctas, smem, s) : launch_t<M, true, false, false>(a, ctas, smem, s);
-  return wx ? launch_t<M, false, true, false>(a, ctas, smem, s) : launch_t<M, false, false, false>(a, ctas, smem, s);
+  if (a.lam_mode == kLamSmem)
+    return wx ? launch_t<M, kLamSmem, true, KIND>(a, ctas, smem, s) : launch_t<M, kLamSmem, false, KIND>(a, ctas, smem, s);
+  // kLamHot, and kLamGlobal as its special case lam_hot = 0 (every label read from global memory)
+  GradArgs b = a;
+  if (a.lam_mode != kLamHot) b.lam_hot = 0;
+  return wx ? launch_t<M, kLamHot, true, KIND>(b, ctas, smem, s) : launch_t<M, kLamHot, false, KIND>(b, ctas, smem, s);
 }
 
 }  // namespace
 
-// one translation unit per family count (grad_m<M>.cu), compiled in parallel
+// one translation unit per (family count, polytope kind): grad_m<M>_k<KIND>.cu, compiled in parallel
 template <>
-cudaError_t launch_fused_grad_m<DL_GRAD_M>(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
-  return launch_m<DL_GRAD_M>(a, ctas, smem, s);
+cudaError_t launch_fused_grad_mk<DL_GRAD_M, DL_GRAD_KIND>(const GradArgs& a, int ctas, size_t smem, cudaStream_t s) {
+  return launch_k<DL_GRAD_M, DL_GRAD_KIND>(a, ctas, smem, s);
 }
 
 }  // namespace dl

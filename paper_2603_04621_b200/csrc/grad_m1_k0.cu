@@ -1,0 +1,4 @@
+// Fused dual-gradient kernels for m = 1 families, polytope kind 0 (see grad_impl.cuh).
+#define DL_GRAD_M 1
+#define DL_GRAD_KIND 0
+#include "grad_impl.cuh"

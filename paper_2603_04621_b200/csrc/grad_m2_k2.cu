@@ -1,0 +1,4 @@
+// Fused dual-gradient kernels for m = 2 families, polytope kind 2 (see grad_impl.cuh).
+#define DL_GRAD_M 2
+#define DL_GRAD_KIND 2
+#include "grad_impl.cuh"

@@ -23,7 +23,14 @@ constexpr int kWarps = 16;         // warps per CTA of the fused kernel
 constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
 constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
-constexpr int kMetaBytes = 768;    // per warp: 2 descriptor-chunk slots (128 B) + 2 rel slots (128 B) + candidate list (256 B)
+// per-warp metadata in shared memory: 2 descriptor-chunk slots (2 x 128 B) + 2 block-offset slots
+// (2 x 128 B) + the kind's candidate structures: simplex -> the warp's candidate list (kListCap
+// entries: u16 tile offset + u8 group slot) and kGSlots group records; box kinds -> a 256-B list
+constexpr int kListCap = 256;
+constexpr int kGSlots = 32;
+constexpr int kMetaSimplex = 512 + kListCap * 3 + kGSlots * 16;  // 1792
+constexpr int kMetaBox = 768;
+inline int meta_bytes(int kind) { return kind == DL_PROJ_SIMPLEX ? kMetaSimplex : kMetaBox; }
 
 struct alignas(16) Tile {
   int64_t off;     // first entry (multiple of kAlign)
@@ -57,8 +64,18 @@ inline int big_phase_of(int bucket) {  // bucket >= 12 -> phase 0 (16 warps) ...
 }
 
 Plan make_plan(const int64_t* row_ptr, int64_t num_sources, int32_t tile_cap);
-int32_t tile_cap_rule(int32_t m, int32_t J, int* lambda_in_smem);
-size_t fused_smem_bytes(int32_t m, int32_t J, int32_t tile_cap, int lambda_in_smem);
+// lambda placement of the fused kernel: kLamGlobal -> every dual read
+// from global memory (L2); kLamSmem -> all m*J duals staged in shared memory; kLamHot -> the
+// duals of destination labels [0, hot) staged (labels = popularity order, R15), the rest global
+enum { kLamGlobal = 0, kLamSmem = 1, kLamHot = 2 };
+struct SmemRule {
+  int32_t tile_cap;
+  int32_t lam_mode;
+  int32_t hot;  // labels cached per family (J for kLamSmem)
+};
+SmemRule smem_rule(int32_t m, int32_t J, int32_t kind);
+size_t fused_smem_bytes(int32_t m, int32_t kind, int32_t tile_cap, int32_t hot);
+int32_t tile_cap_rule(int32_t m, int32_t J, int* lambda_in_smem);  // = smem_rule(m, J, simplex)
 
 void set_error(const std::string& msg);
 
@@ -75,12 +92,6 @@ struct AgdDev {
 };
 
 // ---- kernel launch interfaces (implemented in grad.cu / step.cu) ----------
-struct DeferEntry {  // a short simplex block handed from the fused kernel to deferred_kernel
-  int64_t off;       // first entry in the permuted arrays
-  int32_t b;         // block (layout order)
-  int32_t len;
-};
-
 struct GradArgs {
   const int32_t* dest;
   const float* c;
@@ -93,26 +104,25 @@ struct GradArgs {
   const float* vsq;        // per block v_i^2, or nullptr
   const float* vinv;       // per block 1/v_i^2 (with vsq)
   const int64_t* orig_off; // per block original CSR offset (primal output)
-  const float* lam;        // [m*J]
+  const float* lam;        // [m*J] fp32 duals, indexed by destination LABEL (k*J + label)
   int32_t J, m;
+  int32_t lam_mode;        // kLamGlobal / kLamSmem / kLamHot
+  int32_t lam_hot;         // labels [0, lam_hot) staged in shared memory (kLamHot; J for kLamSmem)
   const double* gamma_ptr; // device gamma (solver) or nullptr -> gamma_val
   double gamma_val;
   double r, u;             // polytope caps (inf where absent)
   int32_t kind;
   int32_t tile_cap;
-  int32_t lam_smem;
-  double* acc;             // [m*J + 4]
-  int32_t* ctr;            // [8] work-queue counters (zeroed before launch); [6] = deferred blocks
-  DeferEntry* defer;       // deferred-block queue (simplex / box kinds)
-  int32_t defer_cap;
+  double* acc;             // [m*J + 4], rows by label
+  int32_t* ctr;            // [8] work-queue counters (zeroed before launch)
   float* x_out;            // primal output (original order) or nullptr
   double* gscratch;        // global fp64 d-scratch for blocks beyond the smem scratch
   int64_t gscratch_per_cta;
 };
 
 cudaError_t launch_fused_grad(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
-template <int M>
-cudaError_t launch_fused_grad_m(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
+template <int M, int KIND>
+cudaError_t launch_fused_grad_mk(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
 
 constexpr int kStepCtas = 64;  // CTAs of the AGD reduce kernel (partials buffer 5 x kStepCtas)
 
@@ -133,33 +143,56 @@ struct StepArgs {
 cudaError_t launch_agd_step(const StepArgs& a, cudaStream_t s);
 
 struct FinalizeArgs {
-  int32_t n;
-  const double* acc;
-  const float* b;
-  const float* lam;
-  double* grad;
+  int32_t n, J;
+  const double* acc;       // label order
+  const float* b;          // label order
+  const float* lam;        // label order
+  const int32_t* lab;      // destination -> label
+  double* grad;            // ORIGINAL order
   double* obj;
   int32_t partial;
 };
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s);
 
+// row norms over the layout (dest = labels) written in ORIGINAL order via unlab
 cudaError_t launch_row_sqnorms(const int32_t* dest, const float* a, int64_t a_stride, int64_t n_entries, int32_t m,
-                               int32_t J, double* out, cudaStream_t s);
-cudaError_t launch_jacobi_diag(const double* rowsq, double* D, int32_t n, cudaStream_t s);
+                               int32_t J, const int32_t* unlab, double* out, cudaStream_t s);
+// D[k*J + lab[j]] = 1/sqrt(rowsq[k*J + j]) (rowsq ORIGINAL order; NULL -> 1)
+cudaError_t launch_jacobi_diag(const double* rowsq, const int32_t* lab, double* D, int32_t m, int32_t J,
+                               cudaStream_t s);
 cudaError_t launch_fill_f64(double* p, double v, int64_t n, cudaStream_t s);
-cudaError_t launch_scale_out(const double* D, const double* lam, double* out, int32_t n, cudaStream_t s);
+// out[k*J + j] = D[k*J + lab[j]] * lam[k*J + lab[j]]  (label order -> ORIGINAL order)
+cudaError_t launch_scale_out(const double* D, const double* lam, const int32_t* lab, double* out, int32_t m,
+                             int32_t J, cudaStream_t s);
+// out[k*J + lab[j]] = in[k*J + j] (f32: ORIGINAL -> label order), and the inverse gather
+cudaError_t launch_permute_f32(const float* in, const int32_t* lab, float* out, int32_t m, int32_t J, int inverse,
+                               cudaStream_t s);
+// relabel an fp64 / fp32 label-ordered vector from labels lab_old to lab_new (via unlab_old)
+cudaError_t launch_relabel_vec_f64(double* v, double* tmp, const int32_t* unlab_old, const int32_t* lab_new,
+                                   int32_t m, int32_t J, cudaStream_t s);
+cudaError_t launch_relabel_vec_f32(float* v, float* tmp, const int32_t* unlab_old, const int32_t* lab_new, int32_t m,
+                                   int32_t J, cudaStream_t s);
+// dest[e] = lab_new[unlab_old[dest[e]]] over the layout
+cudaError_t launch_relabel_dest(int32_t* dest, int64_t n, const int32_t* unlab_old, const int32_t* lab_new,
+                                cudaStream_t s);
+// counts[j] += #edges with dest j (int64), over a raw (original-index) dest array
+cudaError_t launch_dest_histogram(const int32_t* dest, int64_t n, int32_t J, unsigned long long* counts,
+                                  cudaStream_t s);
 
+// Scatter of the caller's CSR sources [i0, i1) into the layout.  The input arrays hold the
+// entries [e0, e0 + n_in) of the CSR (a chunk: a[k * a_in_stride + e - e0]); row_ptr is the full
+// device copy; v (if given) is indexed by source - i0.
 struct LayoutArgs {
   const int64_t* row_ptr;
   const int32_t* dest;
   const float* a;
   const float* c;
   const float* v;
-  int64_t nnz, a_stride_out;
+  int64_t i0, i1, e0, a_in_stride, a_stride_out;
   int32_t m;
-  int64_t num_blocks;
-  const int64_t* perm;
+  const int32_t* blk_of_src;  // block of each source (-1: empty)
   const int64_t* blk_off;
+  const int32_t* lab;         // destination -> label
   int32_t* dest_out;
   float* c_out;
   float* a_out;

@@ -90,27 +90,45 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
   return P;
 }
 
-// Shared memory of the fused kernel: barriers + reduction scratch + (lambda) +
-// 16 warps x 2 stages x tile_cap x (4 B dest + 4 B c + 4 B per family).
+// Shared memory of the fused kernel: barriers + reduction scratch + cached duals +
+// 16 warps x (2 stages x tile_cap x (4 B dest + 4 B c + 4 B per family) + per-warp metadata).
 static constexpr size_t kSmemFixed = 2048 + 1024;  // head + tail pad for over-reads past a tile
 static constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per CTA on sm_100
+static constexpr int kMinTileCap = 256;      // every small block (< 256 entries) fits one tile
 
-size_t fused_smem_bytes(int32_t m, int32_t J, int32_t tile_cap, int lambda_in_smem) {
-  size_t lam = lambda_in_smem ? ((size_t)m * J * 4 + 127) / 128 * 128 : 0;
-  return kSmemFixed + lam + (size_t)kWarps * (2 * tile_cap * (8 + 4 * (size_t)m) + kMetaBytes);
+size_t fused_smem_bytes(int32_t m, int32_t kind, int32_t tile_cap, int32_t hot) {
+  const size_t lam = ((size_t)m * hot * 4 + 127) / 128 * 128;
+  return kSmemFixed + lam + (size_t)kWarps * (2 * (size_t)tile_cap * (8 + 4 * (size_t)m) + meta_bytes(kind));
+}
+
+// lambda placement and tile capacity: all m*J duals in shared memory if
+// that still leaves tiles of >= 256 entries (largest tile 2048); otherwise 256-entry tiles and as
+// many duals of the most popular destination labels as the rest of the 227 KB holds (R15).
+SmemRule smem_rule(int32_t m, int32_t J, int32_t kind) {
+  const int64_t per_entry = (int64_t)kWarps * 2 * (8 + 4 * (int64_t)m);
+  const int64_t fixed = (int64_t)kSmemFixed + (int64_t)kWarps * meta_bytes(kind);
+  SmemRule r{};
+  const int64_t lam_all = ((int64_t)m * J * 4 + 127) / 128 * 128;
+  int64_t cap = ((int64_t)kSmemMax - fixed - lam_all) / per_entry / kAlign * kAlign;
+  if (cap >= kMinTileCap) {
+    r.lam_mode = kLamSmem;
+    r.hot = J;
+    r.tile_cap = (int32_t)std::min<int64_t>(cap, 2048);
+    return r;
+  }
+  r.tile_cap = kMinTileCap;
+  const int64_t budget = (int64_t)kSmemMax - fixed - (int64_t)kMinTileCap * per_entry;
+  int64_t hot = budget / (4 * (int64_t)m) / 32 * 32;
+  hot = std::max<int64_t>(0, std::min<int64_t>(hot, J));
+  r.hot = (int32_t)hot;
+  r.lam_mode = hot > 0 ? kLamHot : kLamGlobal;
+  return r;
 }
 
 int32_t tile_cap_rule(int32_t m, int32_t J, int* lambda_in_smem) {
-  auto cap_for = [&](int lam) -> int64_t {
-    int64_t lamb = lam ? ((int64_t)m * J * 4 + 127) / 128 * 128 : 0;
-    int64_t budget = (int64_t)kSmemMax - (int64_t)kSmemFixed - lamb - (int64_t)kWarps * kMetaBytes;
-    int64_t cap = budget / (kWarps * 2 * (8 + 4 * (int64_t)m));
-    cap = cap / kAlign * kAlign;
-    return std::min<int64_t>(cap, 2048);
-  };
-  int lam = ((int64_t)m * J * 4 <= 96 * 1024 && cap_for(1) >= 256) ? 1 : 0;
-  if (lambda_in_smem) *lambda_in_smem = lam;
-  return (int32_t)std::max<int64_t>(cap_for(lam), 256);
+  SmemRule r = smem_rule(m, J, DL_PROJ_SIMPLEX);
+  if (lambda_in_smem) *lambda_in_smem = r.lam_mode == kLamSmem;
+  return r.tile_cap;
 }
 
 }  // namespace dl

@@ -147,15 +147,17 @@ __global__ void __launch_bounds__(kRedThreads) agd_update_kernel(const StepArgs 
   }
 }
 
-// grad = A x - b (or A x if partial); obj = {g, c^T x, reg, nnz(x)}.
+// grad = A x - b (or A x if partial), un-permuted to ORIGINAL order; obj = {g, c^T x, reg, nnz(x)}.
 __global__ void __launch_bounds__(kStepThreads) finalize_kernel(const FinalizeArgs a) {
   __shared__ double sm[1][32];
   const int n = a.n;
   double v[1] = {0.0};
   for (int r = threadIdx.x; r < n; r += kStepThreads) {
-    const double g = a.partial ? a.acc[r] : a.acc[r] - (double)a.b[r];
+    const int k = r / a.J, j = r - k * a.J;
+    const int l = k * a.J + a.lab[j];
+    const double g = a.partial ? a.acc[l] : a.acc[l] - (double)a.b[l];
     a.grad[r] = g;
-    v[0] += (double)a.lam[r] * g;
+    v[0] += (double)a.lam[l] * g;
   }
   block_sum<1>(v, sm);
   if (threadIdx.x == 0) {
@@ -167,9 +169,9 @@ __global__ void __launch_bounds__(kStepThreads) finalize_kernel(const FinalizeAr
 }
 
 __global__ void row_sqnorms_kernel(const int32_t* dest, const float* a, int64_t a_stride, int64_t n, int32_t m,
-                                   int32_t J, double* out) {
+                                   int32_t J, const int32_t* unlab, double* out) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int j = dest[e];
+    const int j = unlab[dest[e]];
     for (int f = 0; f < m; ++f) {
       const double v = (double)a[f * a_stride + e];
       if (v != 0.0) atomicAdd(out + (size_t)f * J + j, v * v);
@@ -177,10 +179,12 @@ __global__ void row_sqnorms_kernel(const int32_t* dest, const float* a, int64_t 
   }
 }
 
-__global__ void jacobi_diag_kernel(const double* rowsq, double* D, int32_t n) {
+__global__ void jacobi_diag_kernel(const double* rowsq, const int32_t* lab, double* D, int32_t m, int32_t J) {
+  const int n = m * J;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int k = r / J, j = r - k * J;
     const double q = rowsq ? rowsq[r] : 0.0;
-    D[r] = q > 0.0 ? 1.0 / sqrt(q) : 1.0;  // zero rows left unscaled
+    D[k * J + lab[j]] = q > 0.0 ? 1.0 / sqrt(q) : 1.0;  // zero rows left unscaled
   }
 }
 
@@ -189,29 +193,69 @@ __global__ void fill_kernel(double* p, double v, int64_t n) {
     p[i] = v;
 }
 
-__global__ void scale_out_kernel(const double* D, const double* lam, double* out, int32_t n) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) out[r] = D[r] * lam[r];
+__global__ void scale_out_kernel(const double* D, const double* lam, const int32_t* lab, double* out, int32_t m,
+                                 int32_t J) {
+  const int n = m * J;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int k = r / J, l = k * J + lab[r - k * J];
+    out[r] = D[l] * lam[l];
+  }
 }
 
-// One warp per block: copy its entries from the caller's CSR into the layout.
+__global__ void permute_f32_kernel(const float* in, const int32_t* lab, float* out, int32_t m, int32_t J, int inv) {
+  const int n = m * J;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int k = r / J, l = k * J + lab[r - k * J];
+    if (inv) out[r] = in[l];
+    else out[l] = in[r];
+  }
+}
+
+template <class T>
+__global__ void relabel_gather_kernel(const T* v, T* tmp, const int32_t* unlab_old, const int32_t* lab_new, int32_t m,
+                                      int32_t J) {
+  const int n = m * J;  // tmp[k*J + lab_new[j]] = v[k*J + lab_old[j]], j = unlab_old[l_old]
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const int k = r / J, lo = r - k * J;
+    tmp[k * J + lab_new[unlab_old[lo]]] = v[r];
+  }
+}
+
+__global__ void relabel_dest_kernel(int32_t* dest, int64_t n, const int32_t* unlab_old, const int32_t* lab_new) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    dest[e] = lab_new[unlab_old[dest[e]]];
+}
+
+__global__ void dest_histogram_kernel(const int32_t* dest, int64_t n, int32_t J, unsigned long long* counts) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)dest[e];
+    if (j < (uint32_t)J) atomicAdd(counts + j, 1ull);
+  }
+}
+
+// One warp per source of [i0, i1): copy its entries from the caller's CSR chunk into the layout,
+// relabelling destinations.
 __global__ void build_layout_kernel(const LayoutArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t b = w0; b < a.num_blocks; b += nw) {
-    const int64_t i = a.perm[b];
-    const int64_t s0 = a.row_ptr[i], len = a.row_ptr[i + 1] - s0;
+  for (int64_t i = a.i0 + w0; i < a.i1; i += nw) {
+    const int32_t b = a.blk_of_src[i];
+    if (b < 0) continue;
+    const int64_t s0 = a.row_ptr[i] - a.e0, len = a.row_ptr[i + 1] - a.row_ptr[i];
     const int64_t d0 = a.blk_off[b];
     for (int64_t e = lane; e < len; e += 32) {
       const int32_t j = a.dest[s0 + e];
-      if ((uint32_t)j >= (uint32_t)a.J) *a.bad = 1;
-      a.dest_out[d0 + e] = j;
+      if ((uint32_t)j >= (uint32_t)a.J) {
+        *a.bad = 1;
+        continue;
+      }
+      a.dest_out[d0 + e] = a.lab[j];
       a.c_out[d0 + e] = a.c[s0 + e];
-      for (int f = 0; f < a.m; ++f) a.a_out[f * a.a_stride_out + d0 + e] = a.a[f * a.nnz + s0 + e];
+      for (int f = 0; f < a.m; ++f) a.a_out[f * a.a_stride_out + d0 + e] = a.a[f * a.a_in_stride + s0 + e];
     }
-
     if (lane == 0 && a.vsq_out) {
-      const float v = a.v[i];
+      const float v = a.v[i - a.i0];
       a.vsq_out[b] = v * v;
       a.vinv_out[b] = (float)(1.0 / ((double)v * (double)v));
     }
@@ -232,29 +276,62 @@ cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
   finalize_kernel<<<1, kStepThreads, 0, s>>>(a);
   return cudaGetLastError();
 }
+static int grid_for(int64_t n, int64_t cap = 148 * 16) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, cap)); }
 cudaError_t launch_row_sqnorms(const int32_t* dest, const float* a, int64_t a_stride, int64_t n, int32_t m,
-                               int32_t J, double* out, cudaStream_t s) {
+                               int32_t J, const int32_t* unlab, double* out, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  row_sqnorms_kernel<<<blocks, 256, 0, s>>>(dest, a, a_stride, n, m, J, out);
+  row_sqnorms_kernel<<<grid_for(n), 256, 0, s>>>(dest, a, a_stride, n, m, J, unlab, out);
   return cudaGetLastError();
 }
-cudaError_t launch_jacobi_diag(const double* rowsq, double* D, int32_t n, cudaStream_t s) {
-  jacobi_diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(rowsq, D, n);
+cudaError_t launch_jacobi_diag(const double* rowsq, const int32_t* lab, double* D, int32_t m, int32_t J,
+                               cudaStream_t s) {
+  jacobi_diag_kernel<<<grid_for((int64_t)m * J, 4096), 256, 0, s>>>(rowsq, lab, D, m, J);
   return cudaGetLastError();
 }
 cudaError_t launch_fill_f64(double* p, double v, int64_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  fill_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(p, v, n);
+  fill_kernel<<<grid_for(n, 4096), 256, 0, s>>>(p, v, n);
   return cudaGetLastError();
 }
-cudaError_t launch_scale_out(const double* D, const double* lam, double* out, int32_t n, cudaStream_t s) {
-  scale_out_kernel<<<(n + 255) / 256, 256, 0, s>>>(D, lam, out, n);
+cudaError_t launch_scale_out(const double* D, const double* lam, const int32_t* lab, double* out, int32_t m,
+                             int32_t J, cudaStream_t s) {
+  scale_out_kernel<<<grid_for((int64_t)m * J, 4096), 256, 0, s>>>(D, lam, lab, out, m, J);
+  return cudaGetLastError();
+}
+cudaError_t launch_permute_f32(const float* in, const int32_t* lab, float* out, int32_t m, int32_t J, int inverse,
+                               cudaStream_t s) {
+  permute_f32_kernel<<<grid_for((int64_t)m * J, 4096), 256, 0, s>>>(in, lab, out, m, J, inverse);
+  return cudaGetLastError();
+}
+cudaError_t launch_relabel_vec_f64(double* v, double* tmp, const int32_t* unlab_old, const int32_t* lab_new,
+                                   int32_t m, int32_t J, cudaStream_t s) {
+  relabel_gather_kernel<double><<<grid_for((int64_t)m * J, 4096), 256, 0, s>>>(v, tmp, unlab_old, lab_new, m, J);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(v, tmp, (size_t)m * J * sizeof(double), cudaMemcpyDeviceToDevice, s);
+}
+cudaError_t launch_relabel_vec_f32(float* v, float* tmp, const int32_t* unlab_old, const int32_t* lab_new, int32_t m,
+                                   int32_t J, cudaStream_t s) {
+  relabel_gather_kernel<float><<<grid_for((int64_t)m * J, 4096), 256, 0, s>>>(v, tmp, unlab_old, lab_new, m, J);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyAsync(v, tmp, (size_t)m * J * sizeof(float), cudaMemcpyDeviceToDevice, s);
+}
+cudaError_t launch_relabel_dest(int32_t* dest, int64_t n, const int32_t* unlab_old, const int32_t* lab_new,
+                                cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  relabel_dest_kernel<<<grid_for(n, 148 * 32), 256, 0, s>>>(dest, n, unlab_old, lab_new);
+  return cudaGetLastError();
+}
+cudaError_t launch_dest_histogram(const int32_t* dest, int64_t n, int32_t J, unsigned long long* counts,
+                                  cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  dest_histogram_kernel<<<grid_for(n, 148 * 32), 256, 0, s>>>(dest, n, J, counts);
   return cudaGetLastError();
 }
 cudaError_t launch_build_layout(const LayoutArgs& a, cudaStream_t s) {
-  if (a.num_blocks == 0) return cudaSuccess;
-  int blocks = (int)std::min<int64_t>((a.num_blocks * 32 + 255) / 256, 148 * 32);
+  if (a.i1 <= a.i0) return cudaSuccess;
+  int blocks = (int)std::min<int64_t>(((a.i1 - a.i0) * 32 + 255) / 256, 148 * 32);
   build_layout_kernel<<<blocks, 256, 0, s>>>(a);
   return cudaGetLastError();
 }

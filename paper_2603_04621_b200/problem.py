@@ -23,27 +23,36 @@ class MatchingProblem:
                  device=0, stream=None):
         self.device = torch.device("cuda", device)
         dev = self.device
-        t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
-            dev, dt).contiguous()
-        row_ptr = t(row_ptr, torch.int64)
-        dest = t(dest, torch.int32)
-        a = t(a, torch.float32).reshape(-1)
-        c = t(c, torch.float32)
-        b = t(b, torch.float32)
-        v = None if v is None else t(v, torch.float32)
-        self.I = row_ptr.numel() - 1
-        self.J = int(num_dests)
-        self.nnz = int(dest.numel())
-        self.m = a.numel() // max(self.nnz, 1) if self.nnz else b.numel() // self.J
         # the library's work runs on this stream; methods order it against torch's current stream
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
+        on_device = isinstance(dest, torch.Tensor) and dest.is_cuda
+        if on_device:  # CUDA tensors: dl_problem_create reads them in place
+            t = lambda x, dt: (x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))).to(
+                dev, dt).contiguous()
+        else:          # host arrays: dl_problem_create_host streams them into the layout (no device copy)
+            t = lambda x, dt: np.ascontiguousarray(x.cpu().numpy() if isinstance(x, torch.Tensor) else x,
+                                                   dtype=dt)
+        i64, i32, f32 = ((torch.int64, torch.int32, torch.float32) if on_device else (np.int64, np.int32, np.float32))
+        row_ptr = t(row_ptr, i64)
+        dest = t(dest, i32)
+        a = t(a, f32).reshape(-1)
+        c = t(c, f32)
+        b = t(b, f32)
+        v = None if v is None else t(v, f32)
+        n_el = (lambda x: x.numel()) if on_device else (lambda x: x.size)
+        self.I = n_el(row_ptr) - 1
+        self.J = int(num_dests)
+        self.nnz = int(n_el(dest))
+        self.m = n_el(a) // max(self.nnz, 1) if self.nnz else n_el(b) // self.J
         desc = L.dl_problem_desc(self.I, self.J, self.m, self.nnz, L.ptr(row_ptr), L.ptr(dest), L.ptr(a),
                                  L.ptr(c), L.ptr(b), L.ptr(v), int(kind), float(r), float(u), device,
                                  self.stream.cuda_stream)
         with torch.cuda.device(dev):
-            torch.cuda.current_stream(dev).synchronize()  # inputs written on torch's stream
-            self.h = L.dl_problem_create(desc)
-        self._keep = None  # the library copied everything it needs
+            if on_device:
+                torch.cuda.current_stream(dev).synchronize()  # inputs written on torch's stream
+                self.h = L.dl_problem_create(desc)
+            else:
+                self.h = L.dl_problem_create_host(desc)
         self.info = L.dl_problem_get_info(self.h)
         self.n = self.m * self.J
 
@@ -108,6 +117,15 @@ class MatchingProblem:
     def agd_init(self, **kw):
         L.dl_agd_init(self.h, **kw)
 
+    def point(self):
+        """The fp32 dual point mu_t the next evaluation uses (original coordinates)."""
+        mu = np.zeros(self.n, np.float32)
+        L.dl_agd_point(self.h, mu)
+        return mu
+
+    def dest_labels(self):
+        return L.dl_problem_dest_labels(self.h, self.J)
+
     def solve(self, iters):
         L.dl_solve(self.h, iters)
 
@@ -121,14 +139,19 @@ class MatchingProblem:
         return l1, l2
 
     def comm_init(self, rank, world, group=None):
-        """NCCL communicator bootstrapped through torch.distributed (plumbing)."""
+        """NCCL communicator bootstrapped through torch.distributed (plumbing); world == 1
+        without an initialised process group builds a one-rank communicator directly."""
         import torch.distributed as dist
-        uid = L.dl_comm_unique_id() if rank == 0 else bytes(128)
-        buf = torch.tensor(list(uid), dtype=torch.uint8)
-        if dist.get_backend(group) == "nccl":
-            buf = buf.to(self.device)
-        dist.broadcast(buf, 0, group=group)
-        L.dl_comm_init(self.h, rank, world, bytes(buf.cpu().tolist()))
+        if world == 1 and not (dist.is_available() and dist.is_initialized()):
+            L.dl_comm_init(self.h, 0, 1, L.dl_comm_unique_id())
+        else:
+            uid = L.dl_comm_unique_id() if rank == 0 else bytes(128)
+            buf = torch.tensor(list(uid), dtype=torch.uint8)
+            if dist.get_backend(group) == "nccl":
+                buf = buf.to(self.device)
+            dist.broadcast(buf, 0, group=group)
+            L.dl_comm_init(self.h, rank, world, bytes(buf.cpu().tolist()))
+        self.info = L.dl_problem_get_info(self.h)
 
     def allreduce(self, buf):
         cur = self._in()

@@ -24,7 +24,8 @@ full-row-rank assumption of PAPER.md:229).
 from __future__ import annotations
 
 import dataclasses
-from concurrent.futures import ThreadPoolExecutor
+import multiprocessing as mp
+from concurrent.futures import ProcessPoolExecutor, ThreadPoolExecutor
 
 import numpy as np
 
@@ -108,7 +109,25 @@ def dest_params(cfg: GenConfig) -> dict:
     rho = g.uniform(cfg.rho_lo, cfg.rho_hi, size=(m, J))
     cdf = np.cumsum(p)
     cdf[-1] = 1.0
-    return {"p": p, "cdf": cdf, "v": v, "s": s, "rho": rho}
+    # guide table for the categorical draw: guide[k] = first j with cdf[j] > k / K (a lower bound of
+    # searchsorted(cdf, u, 'right') for u in [k/K, (k+1)/K)); _categorical finishes by stepping up
+    K = 1 << max(10, int(np.ceil(np.log2(8 * J))))
+    guide = np.searchsorted(cdf, np.arange(K, dtype=np.float64) / K, side="right").astype(np.int64)
+    return {"p": p, "cdf": cdf, "guide": guide, "v": v, "s": s, "rho": rho}
+
+
+def _categorical(dp: dict, u: np.ndarray) -> np.ndarray:
+    """searchsorted(cdf, u, side='right'), computed from the guide table (identical result)."""
+    cdf, guide = dp["cdf"], dp["guide"]
+    K = guide.size
+    last = cdf.size - 1
+    j = guide[np.minimum((u * K).astype(np.int64), K - 1)]
+    np.minimum(j, last, out=j)
+    while True:
+        step = (cdf[j] <= u) & (j < last)
+        if not step.any():
+            return j
+        j += step
 
 
 def _powerlaw_cdf(cfg: GenConfig) -> np.ndarray:
@@ -144,7 +163,7 @@ def _gen_chunk(cfg: GenConfig, dp: dict, chunk_id: int):
     src = np.repeat(np.arange(nsrc, dtype=np.int64), deg)
     pos = np.arange(src.size, dtype=np.int64) + src     # spacing index of each draw
     u = (cs[pos] - base[src]) / total[src]
-    j = np.searchsorted(dp["cdf"], u, side="right")
+    j = _categorical(dp, u)
     np.minimum(j, J - 1, out=j)
     keep = np.ones(src.size, dtype=bool)                # merge duplicate (i, j) draws
     if src.size > 1:
@@ -164,6 +183,18 @@ def _gen_chunk(cfg: GenConfig, dp: dict, chunk_id: int):
     return lens, dest, c, a, load
 
 
+_DP_CACHE: dict = {}
+
+
+def _gen_chunk_job(args):
+    """Process-pool worker: one chunk (dest_params cached per process)."""
+    cfg, cid = args
+    dp = _DP_CACHE.get(cfg)
+    if dp is None:
+        dp = _DP_CACHE[cfg] = dest_params(cfg)
+    return _gen_chunk(cfg, dp, cid)
+
+
 def generate_shard(cfg: GenConfig, src_begin: int, src_end: int, threads: int = 8):
     """Sources [src_begin, src_end) of the instance, plus their greedy-load partial.
 
@@ -173,8 +204,12 @@ def generate_shard(cfg: GenConfig, src_begin: int, src_end: int, threads: int = 
     dp = dest_params(cfg)
     c0, c1 = src_begin // cfg.chunk, (max(src_end, src_begin + 1) - 1) // cfg.chunk
     ids = list(range(c0, c1 + 1)) if src_end > src_begin else []
-    with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
-        parts = list(ex.map(lambda cid: _gen_chunk(cfg, dp, cid), ids))
+    if threads > 1 and len(ids) >= 4 * threads:  # many chunks: forked worker processes (numpy holds the GIL)
+        with ProcessPoolExecutor(max_workers=threads, mp_context=mp.get_context("fork")) as ex:
+            parts = list(ex.map(_gen_chunk_job, [(cfg, cid) for cid in ids], chunksize=1))
+    else:
+        with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+            parts = list(ex.map(lambda cid: _gen_chunk(cfg, dp, cid), ids))
     lens_l, dest_l, c_l, a_l = [], [], [], []
     load = np.zeros((cfg.num_families, cfg.num_dests), dtype=np.float64)
     for cid, (lens, dest, c, a, ld) in zip(ids, parts):

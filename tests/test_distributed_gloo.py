@@ -67,7 +67,7 @@ def _worker(rank, world, port, out):
         gamma = gamma_at(cfg, t)
         if gprev is not None and gamma != gprev:
             k = 1
-        mu = (d * lam2).astype(np.float32).astype(np.float64)
+        mu = d * lam2
         ev = dual_eval(Ps, mu, gamma)                       # partial: b is zero on the shard
         buf = torch.from_numpy(np.concatenate([ev.Ax, [ev.cx, ev.reg]]))
         dist.all_reduce(buf)                                 # the ONE collective of the iteration

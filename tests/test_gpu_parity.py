@@ -15,7 +15,7 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a GPU", allow_module_level=True)
 
 from oracle.dual import BOX, BOXCUT, SIMPLEX, Problem, apply_A, dual_eval, row_sqnorms  # noqa: E402
-from oracle.layout import tile_plan  # noqa: E402
+from oracle.layout import dest_labels, tile_plan  # noqa: E402
 from paper_2603_04621_b200 import MatchingProblem  # noqa: E402
 from synth.matching import GenConfig, Instance, generate  # noqa: E402
 
@@ -67,8 +67,13 @@ CASES = {
     "boxcut_powerlaw": (GenConfig(num_sources=1500, num_dests=20000, length_law="powerlaw", max_len=6000,
                                   powerlaw_alpha=1.5, seed=24), BOXCUT, 4.0, 0.6),
     "box_m3": (GenConfig(num_sources=1500, num_dests=200, nnz_per_source=30, num_families=3, seed=25), BOX, 1.0, 0.5),
-    "bigJ_lambda_global": (GenConfig(num_sources=1500, num_dests=60000, nnz_per_source=40, seed=26),
-                           SIMPLEX, 2.0, 1.0),
+    "bigJ_lambda_hot": (GenConfig(num_sources=1500, num_dests=60000, nnz_per_source=40, seed=26),
+                        SIMPLEX, 2.0, 1.0),
+    "bigJ_hot_short_blocks": (GenConfig(num_sources=6000, num_dests=100000, length_law="powerlaw", max_len=300,
+                                        powerlaw_alpha=2.0, seed=34), SIMPLEX, 1.0, 1.0),
+    "bigJ_boxcut_m2": (GenConfig(num_sources=1500, num_dests=30000, nnz_per_source=50, num_families=2, seed=35),
+                       BOXCUT, 3.0, 1.0),
+    "paper_table_like": (GenConfig(num_sources=20000, num_dests=2000, nnz_per_source=10, seed=36), SIMPLEX, 1.0, 1.0),
 }
 
 
@@ -196,3 +201,65 @@ def test_near_flat_pieces(kind, r, u):
     P = Problem.from_instance(inst, kind=kind, r=r, u=(np.inf if kind == SIMPLEX else u))
     check_grad(gp, P, np.zeros(J, np.float32), gamma)
     gp.close()
+
+
+@pytest.mark.parametrize("J,relabel", [(300, False), (60000, True), (100000, True)])
+def test_dest_labels_rule(J, relabel):
+    """Labels bit-exact against oracle.layout.dest_labels; the kernel sees labels, every output is
+    in original coordinates (checked by the parity tests above on the same kinds of problems)."""
+    inst = generate(GenConfig(num_sources=3000, num_dests=J, nnz_per_source=30, seed=60))
+    gp = MatchingProblem.from_instance(inst)
+    assert gp.info["relabeled"] == int(relabel)
+    np.testing.assert_array_equal(gp.dest_labels(), np.array(dest_labels(inst.dest, J, relabel), np.int32))
+    if relabel:
+        assert 0 < gp.info["lambda_hot"] < J
+    else:
+        assert gp.info["lambda_hot"] == J and gp.info["lambda_in_smem"] == 1
+    gp.close()
+
+
+@pytest.mark.parametrize("J", [300, 60000])
+def test_host_create_equals_device_create(J):
+    """dl_problem_create_host (numpy input, streamed in source chunks) builds the same layout and
+    the same gradient as dl_problem_create (CUDA tensors)."""
+    inst = generate(GenConfig(num_sources=5000, num_dests=J, nnz_per_source=40, num_families=2, seed=61))
+    v = np.random.default_rng(3).uniform(0.5, 2.0, inst.num_sources).astype(np.float32)
+    gh = MatchingProblem(inst.row_ptr, inst.dest, inst.a, inst.c, inst.b, J, v=v)
+    gd = MatchingProblem(*(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in
+                           (inst.row_ptr, inst.dest, inst.a, inst.c, inst.b)), J, v=torch.from_numpy(v).cuda())
+    for x, y in zip(gh.layout_data(), gd.layout_data()):
+        np.testing.assert_array_equal(x, y)
+    lam = torch.from_numpy(rand_lambda(np.random.default_rng(4), gh.n, 0.2)).to(DEV)
+    g1, o1 = gh.dual_grad(lam, 0.05)
+    g2, o2 = gd.dual_grad(lam, 0.05)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(g1.cpu().numpy(), g2.cpu().numpy(), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(o1.cpu().numpy(), o2.cpu().numpy(), rtol=1e-12)
+    gh.close()
+    gd.close()
+
+
+def test_standalone_calls_between_solver_steps():
+    """dl_dual_grad / dl_primal between solver iterations use their own accumulator: solve(40) ->
+    dual_grad -> primal -> solve(40) equals an uninterrupted solve(80)."""
+    inst = generate(GenConfig(num_sources=4000, num_dests=300, nnz_per_source=50, seed=62))
+    def run(interleave):
+        gp = MatchingProblem.from_instance(inst)
+        gp.agd_init(gamma0=0.05, use_jacobi=False)
+        from paper_2603_04621_b200 import _lib as L
+        if interleave:
+            gp.solve(40)
+            L.dl_agd_eval(gp.h)                     # a half-done iteration: accumulator full
+            lam = torch.full((gp.n,), 0.3, device=DEV)
+            gp.dual_grad(lam, 0.1)
+            gp.primal(lam, 0.1)
+            L.dl_dual_step(gp.h)
+            gp.solve(39)
+        else:
+            gp.solve(80)
+        h = gp.history()
+        gp.close()
+        return h
+    a, b = run(True), run(False)
+    assert a.size == b.size == 80
+    np.testing.assert_allclose(a["g"], b["g"], rtol=1e-9)

@@ -38,14 +38,14 @@ def test_two_step_worked_example():
     """1x1 LP, a=2, b=1, c=-1, box [0,1], gamma=1, Jacobi D = 1/|a| = 1/2.
     t=0: mu=0 -> x=1, grad=2*1-1=1, G=D*grad=0.5, eta=init=1e-5,
          lam1 = 5e-6, lam2 = lam1 (k=1: no momentum).
-    t=1: mu=fl32(2.5e-6) -> x = 1-2mu, grad = 1-4mu, G = 0.5-2mu;
+    t=1: mu=2.5e-6 (fp64, the paper's AGD) -> x = 1-2mu, grad = 1-4mu, G = 0.5-2mu;
          L = |G-G0|/|lam2-0| = 2mu/5e-6 ~ 1 -> eta = min(1/L, 1e-3) = 1e-3;
          lam1' = lam2 + 1e-3 G; lam2' = lam1' + (1/4)(lam1' - lam1)."""
     P = Problem(1, 1, 1, np.array([0, 1]), np.array([0]), np.array([[2.0]]), np.array([-1.0]),
                 np.array([1.0]), BOX, 1.0, 1.0)
     tr = agd(P, 2, AgdConfig(gamma0=1.0))
     assert tr.eta[0] == 1e-5 and tr.g[0] == -0.5
-    mu = float(np.float32(2.5e-6))
+    mu = 2.5e-6
     G1 = 0.5 - 2 * mu
     assert tr.eta[1] == 1e-3
     lam1_0 = 5e-6
