@@ -17,7 +17,9 @@ blocks out bucket-contiguously in HBM and cuts each bucket into *tiles*
   round (``round_blocks(t)`` blocks) is trimmed to whole rounds, the trimmed
   blocks opening the next tile (no warp round runs with idle block groups);
 * every tile starts at an entry offset that is a multiple of 4 (16-byte TMA
-  alignment); blocks inside a tile are contiguous.
+  alignment); blocks inside a tile are contiguous; a block of bucket PAD_BUCKET <= t <
+  BIG_BUCKET (16..255 entries) occupies its length rounded up to a multiple of 4 (padding
+  entries follow it: 128-bit loads of whole 4-entry groups).
 
 Shard plan ("balanced column split"): rank w of W owns the
 contiguous sources [B_w, B_{w+1}) with B_w the first source whose CSR offset
@@ -28,6 +30,7 @@ from __future__ import annotations
 import math
 
 BIG_BUCKET = 9      # buckets >= 9 (length >= 256) are worked by multi-warp groups
+PAD_BUCKET = 5      # buckets 5..8 store blocks padded to a multiple of ALIGN entries
 ALIGN = 4           # entries (16 bytes of int32/float32)
 
 
@@ -48,14 +51,20 @@ def bucket_plan(lengths):
 
 
 def group_lanes(t: int) -> int:
-    """Lanes cooperating on one block of bucket t: 1 for t<=3, else 2^(t-3), at most 512."""
-    return 1 if t <= 3 else min(2 ** (t - 3), 512)
+    """Lanes cooperating on one block of bucket t < BIG_BUCKET: 1 for t <= 3, 2 for t = 4, else 2^(t-4)."""
+    return 1 if t <= 3 else 2 if t == 4 else 2 ** (t - 4)
 
 
 def round_blocks(t: int) -> int:
     """Blocks of bucket t < BIG_BUCKET one warp works at a time (a "round"): 32 / G with the
-    group widths G of the fused kernel (1 lane for t <= 3, 2, 4, 4, 8, 16 lanes for t = 4..8)."""
-    return 32 // {1: 1, 2: 1, 3: 1, 4: 2, 5: 4, 6: 4, 7: 8, 8: 16}[t]
+    group widths G of the fused kernel (1 lane for t <= 3, 2, 2, 4, 8, 16 lanes for t = 4..8)."""
+    return 32 // group_lanes(t)
+
+
+def stored_len(s: int) -> int:
+    """Entries a block of length s occupies in the layout (padded to ALIGN in buckets 5..8)."""
+    t = bucket_of(s)
+    return (s + ALIGN - 1) // ALIGN * ALIGN if PAD_BUCKET <= t < BIG_BUCKET else s
 
 
 def tile_plan(lengths, tile_cap: int):
@@ -79,8 +88,8 @@ def tile_plan(lengths, tile_cap: int):
             q = 0
             while q < len(members):
                 n, tot = 0, 0
-                while q + n < len(members) and (n == 0 or tot + int(lengths[members[q + n]]) <= tile_cap):
-                    tot += int(lengths[members[q + n]])
+                while q + n < len(members) and (n == 0 or tot + stored_len(int(lengths[members[q + n]])) <= tile_cap):
+                    tot += stored_len(int(lengths[members[q + n]]))
                     n += 1
                 if n > R and q + n < len(members):   # trim to whole rounds (the bucket's last tile keeps all)
                     n -= n % R
@@ -92,7 +101,7 @@ def tile_plan(lengths, tile_cap: int):
             for i in grp:
                 perm.append(i)
                 blk_off.append(off)
-                off += int(lengths[i])
+                off += stored_len(int(lengths[i]))
             tiles.append((b0, len(grp), start, off - start, t))
     return perm, blk_off, tiles, off
 
@@ -132,5 +141,5 @@ def shard_bounds(row_ptr, world: int):
     return out
 
 
-__all__ = ["BIG_BUCKET", "ALIGN", "bucket_of", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
+__all__ = ["BIG_BUCKET", "PAD_BUCKET", "ALIGN", "bucket_of", "stored_len", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
            "dest_labels", "shard_bounds"]

@@ -1034,35 +1034,27 @@ __device__ void small_tile(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
 }
 
 // ---------------------------------------------------------------- phase 2: short simplex blocks
-// Candidate-parallel exact projection onto {x >= 0, sum x <= r} (Eq. 4-5).
+// Exact projection onto {x >= 0, sum x <= r} (Eq. 4-5) of every block of a tile.
 //
-// A warp works a tile of short blocks in rounds of NG = 32/G blocks, G = 2^LG lanes per block,
-// E slots per lane (slot k of lane q = block entry q + k G):
-//  1. fp32 pass: s32 = fl(c + sum_k a_k lambda_k) for every slot, group minimum ref;
+// A warp works a tile of short blocks in rounds of NG = 32/G blocks, G = 2^LG lanes per block:
+//  1. fp32 pass: s32 = fl(c + sum_k a_k lambda_k) for every slot, block minimum ref.  Buckets
+//     t <= 3 (<= 7 entries): one lane per block, E slots of consecutive entries; t = 4: two lanes,
+//     slot k of lane q = entry q + 2k.  Buckets 5..8
+//     (stored padded to 4 entries): G = 2^(t-4) lanes, each reading four 4-entry groups with
+//     128-bit loads (slot k of lane q = entry 4 (q + (k/4) G) + k%4);
 //  2. window: only entries with s - s_min < gamma_i r can be positive (x_j > 0 needs d_j < phi* <=
 //     r + d_min); the fp32 filter s32 <= ref + gamma_i r (1 + 1e-6) + slack keeps all of them
 //     (slack bounds the fp32 rounding, R7/R14);
-//  3. the round's candidates (tile offset, group slot) are appended to a per-warp list in shared
-//     memory, one record per group (block, ref, its run in the list);
-//  4. flush (list full, group slots used up, or end of tile): the list is solved 32 candidates at
-//     a time, ONE CANDIDATE PER LANE, in chunks that hold whole blocks: exact fp64 rescoring
-//     d = (c + sum a lambda - ref)/gamma_i, then the closed form of the simplex threshold
-//         phi* = min_k (r + sum of the k smallest d) / k
-//     (the classical sort-and-threshold rule theta = max_k (sum_{i<=k} y_(i) - r)/k in the d frame,
-//     minimised over tie-group ends: rank_j = #{d <= d_j}, S_j = sum{d <= d_j}), threshold
-//     min(phi_free, phi*), x_j = max(threshold - d_j, 0); x > 0 is scattered (red.global.add.f64).
-//  Blocks with more than 32 candidates (large gamma) are solved right after their round by the
-//  whole warp (fp64 Michelot over the block's window, <= 8 entries per lane).
-struct ListSmem {  // per-warp candidate list and group records (meta + 512, kMetaSimplex bytes)
-  uint16_t e[kListCap];      // tile-relative entry
-  uint8_t g[kListCap];       // group slot
-  float ref[kGSlots];        // frame origin (fp32 block minimum)
-  int32_t blk[kGSlots];      // block (layout order)
-  uint16_t start[kGSlots];   // tile-relative first entry of the block
-  uint16_t lo[kGSlots];      // first list index of the block's candidates
-  uint8_t cnt[kGSlots];      // candidates of the block (<= 32)
-};
-static_assert(sizeof(ListSmem) + 512 <= kMetaSimplex, "candidate list fits the simplex metadata");
+//  3. the window's candidates are rescored exactly in fp64, d = (c + sum a lambda - ref)/gamma_i,
+//     and the threshold phi* of F(phi) = sum max(phi - d, 0) = r is found by Michelot's iteration
+//     (phi = (r + sum_S d)/|S| over S = {d < phi}, from S = all candidates, until |S| is stable):
+//     one lane per block works on its own candidates (no shuffles); wider groups compact their
+//     candidates so that lane q owns candidates q, q + G, .. (<= CAP) and sum over the group
+//     with butterflies -- every group of the round iterates at once;
+//  4. threshold min(phi_free, phi*) (theta = 0 exactly when the clamp alone is feasible),
+//     x = max(threshold - d, 0), x > 0 scattered with red.global.add.f64.
+//  Blocks with more candidates than the group holds (large gamma) are solved right after their
+//  round by the whole warp (fp64 Michelot over the block's window, <= 8 entries per lane).
 
 template <int M, int LM, bool WX>
 __device__ __forceinline__ float score32_smem(const Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
@@ -1074,12 +1066,12 @@ __device__ __forceinline__ float score32_smem(const Ctx<M, LM, WX>& C, const int
   return sv;
 }
 
-// The whole warp solves one short block [start, end) of the stage (<= 255 entries, > 32 candidates):
-// window filter as in the pass, exact fp64 d of the candidates, fp64 Michelot.
+// The whole warp solves one short block [start, end) of the stage (<= 256 stored entries): window
+// filter as in the pass, exact fp64 d of the candidates, fp64 Michelot.
 template <int M, int LM, bool WX>
-__device__ __noinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
-                                                const float* sa, int cap, int start, int end, int b, float ref,
-                                                float thr, double vs, double ginv, int lane) {
+__device__ __forceinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
+                                                   const float* sa, int cap, int start, int end, int b, float ref,
+                                                   float thr, double vs, double ginv, int lane) {
   double d64[8];
   uint32_t vm = 0;
   const double refd = (double)ref;
@@ -1096,9 +1088,9 @@ __device__ __noinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int32_t
   });
 }
 
-template <int M, int LM, bool WX, int LG, int E>
+template <int M, int LM, bool WX, int LG, int E, bool V4, int CAP>
 __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
-                                   const uint16_t* rel_s, ListSmem& L, const double* rcp_s) {
+                                   const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
   constexpr int G = 1 << LG;
   constexpr int NG = 32 >> LG;
   const GradArgs& p = C.p;
@@ -1109,30 +1101,70 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
   const int gi = lane >> LG, q = lane & (G - 1);
   const int nrounds = (tl.nb + NG - 1) / NG;
   const double r = p.r;
-  int nlist = 0, ngs = 0;  // warp-uniform fill of the list and of the group slots
-  for (int rd = 0; rd <= nrounds; ++rd) {
-    const bool last = rd == nrounds;
-    // ---- pass + window of round rd (registers: s32 die once the mask is formed)
-    uint32_t cm = 0;
-    int nc = 0, tg = 0, start = 0, end = 0, b = 0;
-    bool active = false;
-    float ref = 0.f, thr = 0.f;
-    if (!last) {
-      const int bb = rd * NG + gi;
-      active = bb < tl.nb;
-      b = tl.b0 + bb;
-      if (active) {
-        if (tl.rel_off >= 0) {
-          start = rel_s[bb];
-          end = rel_s[bb + 1];
-        } else {
-          start = (int)__ldg(p.blk_rel + b);
-          end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
+  for (int rd = 0; rd < nrounds; ++rd) {
+    const int bb = rd * NG + gi;
+    const bool active = bb < tl.nb;
+    const int b = tl.b0 + bb;
+    int start = 0, end = 0;
+    if (active) {
+      if (tl.rel_off >= 0) {
+        start = rel_s[bb];
+        end = rel_s[bb + 1];
+      } else {
+        start = (int)__ldg(p.blk_rel + b);
+        end = bb + 1 < tl.nb ? (int)__ldg(p.blk_rel + b + 1) : tl.nnz;
+      }
+    }
+    double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
+    if (p.vsq && active) {
+      vs = (double)__ldg(p.vsq + b);
+      ginv = C.invgamma * (double)__ldg(p.vinv + b);
+    }
+    // ---- 1. fp32 pass
+    float s32[E];
+    float lmin = kInfF, lmag = 0.f;
+    if constexpr (V4) {
+      // 4-entry groups: lane q reads groups q, q + G, q + 2G, q + 3G of the (padded) block with
+      // 128-bit loads; padding has c = +inf, a = 0, so its score is +inf without a test
+      static_assert(E == 16, "four 4-entry groups per lane");
+      const int ng = (end - start) >> 2;
+#pragma unroll
+      for (int jg = 0; jg < 4; ++jg) {
+        const int g4 = q + jg * G;
+        const int ee = start + 4 * g4;
+        int4 d4 = make_int4(0, 0, 0, 0);
+        float4 c4 = make_float4(kInfF, kInfF, kInfF, kInfF);
+        float4 a4[M];
+#pragma unroll
+        for (int f = 0; f < M; ++f) a4[f] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (g4 < ng) {
+          d4 = *reinterpret_cast<const int4*>(sd + ee);
+          c4 = *reinterpret_cast<const float4*>(sc + ee);
+#pragma unroll
+          for (int f = 0; f < M; ++f) a4[f] = *reinterpret_cast<const float4*>(sa + f * cap + ee);
+        }
+        const int jj[4] = {d4.x, d4.y, d4.z, d4.w};
+        float sv[4] = {c4.x, c4.y, c4.z, c4.w}, mg[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) mg[c] = fabsf(sv[c]);
+#pragma unroll
+        for (int f = 0; f < M; ++f) {
+          const float av[4] = {a4[f].x, a4[f].y, a4[f].z, a4[f].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float lv = C.lam(f, jj[c]);
+            sv[c] = fmaf(av[c], lv, sv[c]);
+            if constexpr (M > 1) mg[c] = fmaf(fabsf(av[c]), fabsf(lv), mg[c]);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          s32[4 * jg + c] = sv[c];
+          lmin = fminf(lmin, sv[c]);
+          if constexpr (M > 1) lmag = sv[c] < kInfF ? fmaxf(lmag, mg[c]) : lmag;
         }
       }
-      const double vs = (p.vsq && active) ? (double)__ldg(p.vsq + b) : 1.0;
-      float s32[E];
-      float lmin = kInfF, lmag = 0.f;
+    } else {  // scalar slots: slot k of lane q = entry start + q + k G
       const int lim = (end - start) - q;
 #pragma unroll
       for (int k = 0; k < E; ++k) {
@@ -1150,137 +1182,149 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
         lmin = fminf(lmin, sv);
         if constexpr (M > 1) lmag = sv < kInfF ? fmaxf(lmag, mg) : lmag;
       }
-      ref = tmin<G>(lmin);
-      const float gr = (float)(r * C.gamma * vs);
-      // fp32 rounding bound of s_j - ref and the threshold (as r01, K1 step 2)
-      const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
-      thr = ref + (gr * 1.000001f + slack);
+    }
+    const float ref = tmin<G>(lmin);
+    // ---- 2. window (fp32 rounding bound of s_j - ref and of the threshold, K1 step 2)
+    const float gr = (float)(r * C.gamma * vs);
+    const float slack = M == 1 ? 4.7683716e-7f * (fabsf(ref) + gr) : 2.3841858e-7f * (M + 1) * tmax<G>(lmag);
+    const float thr = ref + (gr * 1.000001f + slack);
+    uint32_t cm = 0;
 #pragma unroll
-      for (int k = 0; k < E; ++k)
-        if (s32[k] <= thr) cm |= 1u << k;
-      if (!active) cm = 0;
-      nc = __popc(cm);
-      tg = tsum<G>(nc);
-      if (tg > 32) cm = 0, nc = 0;  // solved by the whole warp after the round
-    }
-    // warp-wide exclusive prefix of the candidate counts (lane order = group order)
-    int incl = nc;
+    for (int k = 0; k < E; ++k)
+      if (s32[k] <= thr) cm |= 1u << k;
+    if (!active) cm = 0;
+    // ---- 3. candidates in registers: lane-local (G = 1) or compacted over the group
+    const int nc = __popc(cm);
+    int excl = 0, T = nc;
+    if constexpr (G > 1) {
+      int incl = nc;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(kFull, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int total = __shfl_sync(kFull, incl, 31);
-    // ---- flush: solve the list (before this round's candidates are written)
-    if (last || nlist + total > kListCap || ngs + NG > kGSlots) {
-      __syncwarp();
-      for (int base = 0; base < nlist;) {
-        const int i = base + lane;
-        const bool valid = i < nlist;
-        const int g = valid ? L.g[i] : 0;
-        const int lo = L.lo[g], n = L.cnt[g];
-        const unsigned nf = __ballot_sync(kFull, valid && lo + n > base + 32);
-        const int endc = nf ? __shfl_sync(kFull, lo, __ffs(nf) - 1) : min(nlist, base + 32);
-        const bool act = i < endc;
-        const int b_g = L.blk[g];
-        const double vs = p.vsq ? (double)__ldg(p.vsq + b_g) : 1.0;
-        const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + b_g) : C.invgamma;
-        const double refd = (double)L.ref[g];
-        const int e = L.e[valid ? i : 0];
-        const double d = act ? (score_smem(C, sd, sc, sa, cap, e) - refd) * ginv : 0.0;
-        // rank and prefix sum of d inside the block's run of lanes [lo - base, lo - base + n)
-        const int sl = lo - base;
-        const int nmax = (int)__reduce_max_sync(kFull, act ? (unsigned)n : 0u);
-        int rank = 0;
-        double S = 0.0;
-        for (int o = 0; o < nmax; ++o) {
-          const int src = act ? sl + min(o, n - 1) : lane;
-          const double dd = __shfl_sync(kFull, d, src);
-          if (act && o < n && dd <= d) {
-            ++rank;
-            S += dd;
-          }
-        }
-        const double f = (r + S) * rcp_s[act ? rank : 1];
-        double phi = f;
-        for (int o = 0; o < nmax; ++o) {
-          const int src = act ? sl + min(o, n - 1) : lane;
-          phi = fmin(phi, __shfl_sync(kFull, f, src));
-        }
-        if (act) {
-          const double x = fmax(fmin(-refd * ginv, phi) - d, 0.0);
-          if (x > 0.0) emit_smem(C, sd, sc, sa, cap, e, x, vs, b_g, e - L.start[g]);
-        }
-        base = endc;
+      for (int o = 1; o < G; o <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, o, G);
+        if (q >= o) incl += v;
       }
-      nlist = 0;
-      ngs = 0;
-      __syncwarp();
+      T = __shfl_sync(kFull, incl, G - 1, G);
+      excl = incl - nc;
     }
-    if (last) break;
-    // ---- append this round's candidates and group records
-    {
-      int pos = nlist + incl - nc;
-      uint32_t m = cm;
-      while (m) {
-        const int k = __ffs(m) - 1;
-        m &= m - 1;
-        L.e[pos] = (uint16_t)(start + q + k * G);
-        L.g[pos] = (uint8_t)(ngs + gi);
-        ++pos;
+    const bool over = T > CAP * G;  // group-uniform
+    const double refd = (double)ref;
+    double d64[CAP];
+    int ei[CAP];
+    int own = 0;
+    if constexpr (G == 1) {
+      uint32_t m = over ? 0u : cm;
+#pragma unroll
+      for (int c = 0; c < CAP; ++c) {
+        d64[c] = kInfD;
+        ei[c] = 0;
+        if (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          ei[c] = start + k;  // G = 1: slot k is entry k
+          d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
+          ++own;
+        }
       }
-      if (q == 0) {
-        const int gs = ngs + gi;
-        L.ref[gs] = ref;
-        L.blk[gs] = b;
-        L.start[gs] = (uint16_t)start;
-        L.lo[gs] = (uint16_t)(nlist + incl - nc);
-        L.cnt[gs] = (uint8_t)(active && tg <= 32 ? tg : 0);
+    } else {
+      uint16_t* lst = cand_s + gi * (CAP * G);
+      if (!over) {
+        uint32_t m = cm;
+        int o = excl;
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          lst[o++] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
+        }
       }
-      nlist += total;
-      ngs += NG;
       __syncwarp();
+      own = over ? 0 : (T - q + G - 1) >> LG;  // candidates q, q + G, ... of the group
+#pragma unroll
+      for (int c = 0; c < CAP; ++c) {
+        d64[c] = kInfD;
+        ei[c] = 0;
+        if (c < own) {
+          ei[c] = lst[q + c * G];
+          d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
+        }
+      }
+      __syncwarp();  // the list is rewritten by the next round
     }
-    // ---- blocks with > 32 candidates: the whole warp, one block at a time
-    unsigned big = __ballot_sync(kFull, q == 0 && active && tg > 32);
+    // Michelot in fp64 over the group's candidates, every group at once (warp-uniform loop)
+    double sl = 0.0;
+#pragma unroll
+    for (int c = 0; c < CAP; ++c)
+      if (c < own) sl += d64[c];
+    const int Tg = over ? 0 : T;
+    double phi = (r + tsum<G>(sl)) * rcp_s[Tg];
+    int cprev = Tg;
+    bool done = Tg <= 1;
+    for (int it = 0; it < 64 && __any_sync(kFull, !done); ++it) {
+      int cnt = 0;
+      double s2 = 0.0;
+#pragma unroll
+      for (int c = 0; c < CAP; ++c)
+        if (c < own && d64[c] < phi) {
+          ++cnt;
+          s2 += d64[c];
+        }
+      cnt = tsum<G>(cnt);
+      s2 = tsum<G>(s2);
+      if (!done) {
+        if (cnt == cprev || cnt == 0) {
+          done = true;
+        } else {
+          cprev = cnt;
+          phi = (r + s2) * rcp_s[cnt];
+        }
+      }
+    }
+    // ---- 4. threshold and emission
+    const double ph = fmin(-refd * ginv, phi);
+#pragma unroll
+    for (int c = 0; c < CAP; ++c)
+      if (c < own) {
+        const double x = fmax(ph - d64[c], 0.0);
+        if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ei[c], x, vs, b, ei[c] - start);
+      }
+    // ---- blocks whose candidates overflow the registers: the whole warp, one block at a time
+    unsigned big = __ballot_sync(kFull, q == 0 && active && over);
     while (big) {
       const int src = __ffs(big) - 1;
       big &= big - 1;
       const int s0 = __shfl_sync(kFull, start, src), s1 = __shfl_sync(kFull, end, src);
       const int bk = __shfl_sync(kFull, b, src);
       const float rf = __shfl_sync(kFull, ref, src), th = __shfl_sync(kFull, thr, src);
-      const double vs = p.vsq ? (double)__ldg(p.vsq + bk) : 1.0;
-      const double ginv = p.vsq ? C.invgamma * (double)__ldg(p.vinv + bk) : C.invgamma;
-      warp_block_simplex<M, LM, WX>(C, sd, sc, sa, cap, s0, s1, bk, rf, th, vs, ginv, lane);
+      const double vsb = __shfl_sync(kFull, vs, src), gb = __shfl_sync(kFull, ginv, src);
+      warp_block_simplex<M, LM, WX>(C, sd, sc, sa, cap, s0, s1, bk, rf, th, vsb, gb, lane);
     }
   }
 }
 
 template <int M, int LM, bool WX>
 __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
-                                                       int lane, const uint16_t* rel_s, ListSmem& L,
+                                                       int lane, const uint16_t* rel_s, uint16_t* cand_s,
                                                        const double* rcp_s) {
-  switch (tl.bucket) {  // (LG, E): E 2^LG >= every length of bucket t; round_blocks(t) = 32 / 2^LG
-    case 1: small_tile_simplex<M, LM, WX, 0, 1>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 2: small_tile_simplex<M, LM, WX, 0, 3>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 3: small_tile_simplex<M, LM, WX, 0, 7>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 4: small_tile_simplex<M, LM, WX, 1, 8>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 5: small_tile_simplex<M, LM, WX, 2, 8>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 6: small_tile_simplex<M, LM, WX, 2, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    case 7: small_tile_simplex<M, LM, WX, 3, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
-    default: small_tile_simplex<M, LM, WX, 4, 16>(C, tl, stage, lane, rel_s, L, rcp_s); break;
+  switch (tl.bucket) {  // (LG, E, V4, CAP): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
+    case 1: small_tile_simplex<M, LM, WX, 0, 1, false, 1>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 2: small_tile_simplex<M, LM, WX, 0, 3, false, 3>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 3: small_tile_simplex<M, LM, WX, 0, 7, false, 6>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 4: small_tile_simplex<M, LM, WX, 1, 8, false, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 5: small_tile_simplex<M, LM, WX, 1, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 6: small_tile_simplex<M, LM, WX, 2, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 7: small_tile_simplex<M, LM, WX, 3, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    default: small_tile_simplex<M, LM, WX, 4, 16, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
   }
 }
 
 template <int M, int LM, bool WX, bool GEN>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
                                                const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
-  switch (tl.bucket) {  // (LG, E): E 2^LG > every length of bucket t
+  switch (tl.bucket) {  // (LG, E): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
     case 1:
     case 2:
     case 3: small_tile<M, LM, WX, 0, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 4: small_tile<M, LM, WX, 1, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 5: small_tile<M, LM, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 5: small_tile<M, LM, WX, 1, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 6: small_tile<M, LM, WX, 2, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 7: small_tile<M, LM, WX, 3, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     default: small_tile<M, LM, WX, 4, 16, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
@@ -1355,12 +1399,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     constexpr int kChunk = 4;
     const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
     char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
-    constexpr int kMeta = KIND == DL_PROJ_SIMPLEX ? kMetaSimplex : kMetaBox;
+    constexpr int kMeta = kMetaBytes;
     char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMeta;
     const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
     const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
-    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // box kinds: [128] candidate list
-    ListSmem& lsm = *reinterpret_cast<ListSmem*>(meta + 512);               // simplex: candidate list
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // [128] candidate list
     uint64_t* bars = head->mbar[warp];
     uint64_t* dbars = head->mbar_desc[warp];
     if (lane == 0) {
@@ -1435,7 +1478,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       mbar_wait(&bars[st], (phase >> st) & 1u);
       phase ^= 1u << st;
       if constexpr (KIND == DL_PROJ_SIMPLEX)
-        small_dispatch_simplex<M, LM, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, lsm,
+        small_dispatch_simplex<M, LM, WX>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,
                                           head->rcp);
       else
         small_dispatch<M, LM, WX, true>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,

@@ -24,13 +24,9 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
 constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
 // per-warp metadata in shared memory: 2 descriptor-chunk slots (2 x 128 B) + 2 block-offset slots
-// (2 x 128 B) + the kind's candidate structures: simplex -> the warp's candidate list (kListCap
-// entries: u16 tile offset + u8 group slot) and kGSlots group records; box kinds -> a 256-B list
-constexpr int kListCap = 256;
-constexpr int kGSlots = 32;
-constexpr int kMetaSimplex = 512 + kListCap * 3 + kGSlots * 16;  // 1792
-constexpr int kMetaBox = 768;
-inline int meta_bytes(int kind) { return kind == DL_PROJ_SIMPLEX ? kMetaSimplex : kMetaBox; }
+// (2 x 128 B) + the round's compacted candidate list (128 x u16)
+constexpr int kMetaBytes = 768;
+inline int meta_bytes(int) { return kMetaBytes; }
 
 struct alignas(16) Tile {
   int64_t off;     // first entry (multiple of kAlign)
@@ -54,11 +50,17 @@ struct Plan {
 };
 
 inline int bucket_of(int64_t s) { return 64 - __builtin_clzll((unsigned long long)s); }
-// blocks of a small bucket one warp works per round: 32 / G, G the group width of the fused
-// kernel (small_dispatch: 1 lane for t <= 3, then 2, 4, 4, 8, 16 lanes for t = 4..8)
-inline int round_blocks(int bucket) {
-  return bucket <= 3 ? 32 : bucket == 4 ? 16 : bucket <= 6 ? 8 : bucket == 7 ? 4 : 2;
+// buckets [kPadBucket, kBigBucket) (16..255 entries) store every block padded to a multiple of
+// kAlign entries (padding: label 0, c = +inf, a = 0) so that the fused kernel reads them 4 entries
+// per 128-bit shared-memory load
+constexpr int kPadBucket = 5;
+inline int64_t stored_len(int64_t s) {
+  const int t = bucket_of(s);
+  return (t >= kPadBucket && t < kBigBucket) ? (s + kAlign - 1) / kAlign * kAlign : s;
 }
+// blocks of a small bucket one warp works per round: 32 / G, G the group width of the fused
+// kernel (1 lane for t <= 3, then 2, 2, 4, 8, 16 lanes for t = 4..8)
+inline int round_blocks(int bucket) { return bucket <= 3 ? 32 : bucket == 4 ? 16 : 32 >> (bucket - 4); }
 inline int big_phase_of(int bucket) {  // bucket >= 12 -> phase 0 (16 warps) ... 9 -> phase 3 (2 warps)
   return bucket >= 12 ? 0 : 12 - bucket;
 }

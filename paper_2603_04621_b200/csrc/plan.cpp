@@ -55,7 +55,7 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
       int64_t n = 0, tot = 0;
       while (b + n < end) {
         const int64_t i = P.perm[b + n];
-        const int64_t s = row_ptr[i + 1] - row_ptr[i];
+        const int64_t s = stored_len(row_ptr[i + 1] - row_ptr[i]);
         if (n > 0 && (big || tot + s > tile_cap)) break;
         tot += s;
         ++n;
@@ -68,8 +68,8 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
       Tile& tl = P.tiles.back();
       for (int64_t q = 0; q < n; ++q, ++b) {
         const int64_t i = P.perm[b];
-        const int64_t s = row_ptr[i + 1] - row_ptr[i];
-        P.max_len = std::max<int32_t>(P.max_len, (int32_t)s);
+        P.max_len = std::max<int32_t>(P.max_len, (int32_t)(row_ptr[i + 1] - row_ptr[i]));
+        const int64_t s = stored_len(row_ptr[i + 1] - row_ptr[i]);
         P.blk_off[b] = off;
         off += s;
         tl.nnz += (int32_t)s;

@@ -254,6 +254,14 @@ __global__ void build_layout_kernel(const LayoutArgs a) {
       a.c_out[d0 + e] = a.c[s0 + e];
       for (int f = 0; f < a.m; ++f) a.a_out[f * a.a_stride_out + d0 + e] = a.a[f * a.a_in_stride + s0 + e];
     }
+    // padding of buckets 5..8 (stored_len): label 0, c = +inf, a = 0 -> never a candidate
+    const int64_t slen = (len >= 16 && len < 256) ? (len + kAlign - 1) / kAlign * kAlign : len;
+    if (lane < slen - len) {
+      const int64_t e = d0 + len + lane;
+      a.dest_out[e] = 0;
+      a.c_out[e] = __int_as_float(0x7f800000);
+      for (int f = 0; f < a.m; ++f) a.a_out[f * a.a_stride_out + e] = 0.f;
+    }
     if (lane == 0 && a.vsq_out) {
       const float v = a.v[i - a.i0];
       a.vsq_out[b] = v * v;

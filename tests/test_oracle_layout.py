@@ -5,7 +5,8 @@ import math
 
 import numpy as np
 
-from oracle.layout import (ALIGN, BIG_BUCKET, bucket_of, bucket_plan, group_lanes, round_blocks, shard_bounds,
+from oracle.layout import (ALIGN, BIG_BUCKET, PAD_BUCKET, bucket_of, bucket_plan, group_lanes, round_blocks,
+                           shard_bounds, stored_len,
                            tile_plan)
 
 
@@ -37,17 +38,25 @@ def test_launch_bound_and_padding_bound():
 
 
 def test_round_blocks_match_group_widths():
-    """round_blocks(t) = 32 / G(t): 32 one-lane groups for t <= 3, 16 two-lane groups for t = 4, ...,
-    2 sixteen-lane groups for t = 8 (E G >= 2^t slots hold every block of the bucket, E <= 16)."""
-    E = {1: 8, 2: 8, 3: 8, 4: 8, 5: 8, 6: 16, 7: 16, 8: 16}
+    """round_blocks(t) = 32 / G(t): 32 one-lane groups for t <= 3, 16 two-lane groups for t = 4, 5,
+    then 8, 4, 2 groups of 4, 8, 16 lanes for t = 6..8; E G >= stored length of every block of the
+    bucket with the kernel's slots per lane E (1, 3, 7 single-lane slots for t <= 3, 8 for t = 4;
+    16 = four 4-entry groups for t >= 5)."""
+    E = {1: 1, 2: 3, 3: 7, 4: 8, 5: 16, 6: 16, 7: 16, 8: 16}
     for t in range(1, BIG_BUCKET):
-        G = 32 // round_blocks(t)
-        assert G * round_blocks(t) == 32 and E[t] * G >= 2 ** t
+        G = group_lanes(t)
+        assert G * round_blocks(t) == 32
+        assert E[t] * G >= stored_len(2 ** t - 1)
 
 
-def test_group_lanes_hold_block_in_8_per_lane():
-    for t in range(1, 13):
-        assert math.ceil((2 ** t - 1) / group_lanes(t)) <= 8
+def test_stored_len_padding():
+    for s in range(1, 600):
+        t = bucket_of(s)
+        p = stored_len(s)
+        if PAD_BUCKET <= t < BIG_BUCKET:
+            assert p % ALIGN == 0 and s <= p < s + ALIGN and bucket_of(p) == t or (p == 2 ** t and s > 2 ** t - ALIGN)
+        else:
+            assert p == s
 
 
 def test_tile_plan_invariants():
@@ -74,8 +83,8 @@ def test_tile_plan_invariants():
             assert all(bucket_of(int(lens[i])) == t for i in members)
             assert off[b0] == toff
             for q in range(nb - 1):
-                assert off[b0 + q + 1] == off[b0 + q] + lens[members[q]]
-            assert tn == sum(int(lens[i]) for i in members)
+                assert off[b0 + q + 1] == off[b0 + q] + stored_len(int(lens[members[q]]))
+            assert tn == sum(stored_len(int(lens[i])) for i in members)
             if t >= BIG_BUCKET:
                 assert nb == 1
             else:
@@ -88,8 +97,8 @@ def test_tile_plan_invariants():
             if a[4] == b[4] and a[4] < BIG_BUCKET:
                 run, tot = 0, 0
                 while a[0] + run < len(perm) and bucket_of(int(lens[perm[a[0] + run]])) == a[4] and \
-                        (run == 0 or tot + lens[perm[a[0] + run]] <= cap):
-                    tot += lens[perm[a[0] + run]]
+                        (run == 0 or tot + stored_len(int(lens[perm[a[0] + run]])) <= cap):
+                    tot += stored_len(int(lens[perm[a[0] + run]]))
                     run += 1
                 R = round_blocks(a[4])
                 assert a[1] == (run if run <= R else run - run % R)
