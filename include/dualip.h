@@ -223,6 +223,13 @@ dl_status dl_comm_init(dl_problem* p, int32_t rank, int32_t world, const void* i
  * (used for row norms / greedy loads at setup). */
 dl_status dl_comm_allreduce(dl_problem* p, double* buf, int64_t n);
 
+/* Diagnostics: with DUALIP_TRACE=1 in the environment at create time, every fused pass records
+ * per CTA {smid, globaltimer at start, after lambda staging, at exit (ns), tiles worked}
+ * (5 x uint64 per CTA), then the globaltimer at which each 4-tile chunk of the short-block phase was
+ * finished (written by the pass itself: the last pass only).  *n = the record count (0 when tracing
+ * is off); copies min(cap, *n) to the HOST buffer out (NULL: size query only).  Synchronous. */
+dl_status dl_debug_trace(dl_problem* p, uint64_t* out, int64_t cap, int64_t* n);
+
 /* Synchronise the problem's stream. */
 dl_status dl_sync(dl_problem* p);
 

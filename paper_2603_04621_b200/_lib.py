@@ -98,6 +98,7 @@ _sig = {
     "dl_comm_unique_id": (C.c_int, [_P]),
     "dl_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     "dl_comm_allreduce": (C.c_int, [_P, _P, C.c_int64]),
+    "dl_debug_trace": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
     "dl_sync": (C.c_int, [_P]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -286,6 +287,17 @@ def dl_comm_init(h, rank, world, uid: bytes):
 
 def dl_comm_allreduce(h, buf, n):
     _ck(_lib.dl_comm_allreduce(h, ptr(buf), int(n)))
+
+
+def dl_debug_trace(h):
+    """Trace of the last fused pass (DUALIP_TRACE=1 at create): uint64, [ctas x 5] per-CTA records, then
+    the completion time of every 4-tile chunk of the short-block phase."""
+    n = C.c_int64()
+    _ck(_lib.dl_debug_trace(h, None, 0, C.byref(n)))
+    out = np.zeros(n.value, np.uint64)
+    if n.value:
+        _ck(_lib.dl_debug_trace(h, ptr(out), n.value, C.byref(n)))
+    return out
 
 
 def dl_sync(h):

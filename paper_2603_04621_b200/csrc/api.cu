@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -79,6 +80,7 @@ struct dl_problem {
   int64_t* d_orig_off = nullptr;
   double* d_gscratch = nullptr;
   int64_t gscratch_per_cta = 0;
+  unsigned long long* d_trace = nullptr;  // per-CTA launch trace of the last fused pass (DUALIP_TRACE=1)
   // destination labels (R15): lab[j] = label of j, unlab = inverse
   bool relabeled = false;
   int32_t *d_lab = nullptr, *d_unlab = nullptr;
@@ -89,6 +91,9 @@ struct dl_problem {
   double* d_step_scal = nullptr;
   // solver work (AGD accumulator) and standalone-gradient work: separate buffers, so a
   // standalone call between solver steps never disturbs the solver's accumulator
+  double* d_part = nullptr;  // per-CTA partial accumulators [part_copies][part_stride] (zero between passes)
+  int64_t part_stride = 0;
+  int32_t part_copies = 1;
   double* d_acc = nullptr;   // [MJ + 4]
   int32_t* d_ctr = nullptr;  // [8]
   double* d_acc_s = nullptr;
@@ -196,7 +201,7 @@ std::vector<int32_t> labels_from_counts(const std::vector<unsigned long long>& c
 }
 
 GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, double gamma_val, float* x_out,
-                   double* acc, int32_t* ctr) {
+                   int32_t* ctr) {
   GradArgs a{};
   a.dest = p->d_dest;
   a.c = p->d_c;
@@ -220,11 +225,14 @@ GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   a.tile_cap = p->tile_cap;
   a.lam_mode = p->lam_mode;
   a.lam_hot = p->lam_hot;
-  a.acc = acc;
+  a.acc = p->d_part;
+  a.acc_stride = p->part_stride;
+  a.acc_copies = p->part_copies;
   a.ctr = ctr;
   a.x_out = x_out;
   a.gscratch = p->d_gscratch;
   a.gscratch_per_cta = p->gscratch_per_cta;
+  a.trace = p->d_trace;
   return a;
 }
 
@@ -235,13 +243,12 @@ dl_status run_grad(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   const int64_t n = (int64_t)p->M * p->J;
   double* acc = standalone ? p->d_acc_s : p->d_acc;
   int32_t* ctr = standalone ? p->d_ctr_s : p->d_ctr;
-  if (standalone) {
-    CUDA_TRY(cudaMemsetAsync(acc, 0, (n + 4) * sizeof(double), p->stream));
-    CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(int32_t), p->stream));
-  }
-  if (p->plan.tiles.empty()) return DL_OK;
-  CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out, acc, ctr), p->ctas, p->smem,
-                             p->stream));
+  if (standalone) CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(int32_t), p->stream));
+  if (!p->plan.tiles.empty())
+    CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out, ctr), p->ctas, p->smem,
+                               p->stream));
+  // the CTA copies -> acc (every row written; the copies are left zero for the next pass)
+  CUDA_TRY(launch_partial_sum(p->d_part, p->part_stride, p->part_copies, n + 4, acc, p->stream));
   return DL_OK;
 }
 
@@ -416,6 +423,12 @@ dl_status create_common(const dl_problem_desc* d, dl_problem** out, bool host) {
       (s = dev_alloc(p, &p->d_tmp, MJ)) || (s = dev_alloc(p, &p->d_lab, J)) || (s = dev_alloc(p, &p->d_unlab, J)))
     return fail(s);
   if (d->v && ((s = dev_alloc(p, &p->d_vsq, nb)) || (s = dev_alloc(p, &p->d_vinv, nb)))) return fail(s);
+  // per-CTA accumulator copies: one per CTA, fewer when m J is
+  // so large that 148 copies would exceed 1 GiB (CTAs then share copies round-robin)
+  p->part_stride = (MJ + 4 + 31) / 32 * 32;
+  p->part_copies = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p->ctas, (int64_t)(1ll << 30) / (p->part_stride * 8)));
+  if ((s = dev_alloc(p, &p->d_part, (size_t)p->part_stride * p->part_copies))) return fail(s);
+  CREATE_TRY(cudaMemsetAsync(p->d_part, 0, (size_t)p->part_stride * p->part_copies * sizeof(double), p->stream));
   // global d-scratch for blocks longer than a 16-warp group's shared scratch
   const int64_t smem_scr = (int64_t)kWarps * 2 * p->tile_cap * (8 + 4 * p->M) / 8;  // fp64 d
   if (P.max_len > smem_scr) {
@@ -596,6 +609,8 @@ dl_status create_common(const dl_problem_desc* d, dl_problem** out, bool host) {
   CREATE_TRY(launch_jacobi_diag(nullptr, p->d_lab, p->d_Dones, p->M, p->J, p->stream));
   CREATE_TRY(cudaStreamSynchronize(p->stream));
   for (auto& t : temps) dev_release(p, t.first, t.second);
+  if (const char* tr = std::getenv("DUALIP_TRACE"))
+    if (tr[0] == '1' && (s = dev_alloc(p, &p->d_trace, (size_t)p->ctas * 5 + (size_t)nt / 4 + 8))) return fail(s);
 #undef CREATE_TRY
   *out = p;
   return DL_OK;
@@ -1082,6 +1097,19 @@ dl_status dl_comm_allreduce(dl_problem* p, double* buf, int64_t n) {
     set_error("ncclAllReduce failed");
     return DL_ERR_NCCL;
   }
+  return DL_OK;
+}
+
+dl_status dl_debug_trace(dl_problem* p, uint64_t* out, int64_t cap, int64_t* n) {
+  if (!p || !n) {
+    set_error("dl_debug_trace: NULL");
+    return DL_ERR_INVALID;
+  }
+  *n = p->d_trace ? (int64_t)p->ctas * 5 + (int64_t)p->plan.tiles.size() / 4 + 8 : 0;
+  if (!p->d_trace || !out) return DL_OK;
+  DeviceGuard guard(p->device);
+  CUDA_TRY(cudaMemcpyAsync(out, p->d_trace, (size_t)std::min(cap, *n) * 8, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(cudaStreamSynchronize(p->stream));
   return DL_OK;
 }
 

@@ -9,6 +9,9 @@
 //          phi the threshold of the block polytope (R1, R7)
 //   acc[k*J + j] += a_kij x_ij   (fp64 red.global, only where x_ij > 0)
 //   acc[mJ+0] += c_ij x_ij, acc[mJ+1] += gamma_i/2 x_ij^2, acc[mJ+2] += [x_ij > 0]
+// into the CTA's own copy of the accumulator (launch_partial_sum adds the copies): reductions from
+// every SM onto one shared m*J array put the B200 into a state where the whole pass streams ~1.6x
+// slower; CTA-private rows do not.
 //
 // Work = the tile list of the layout (plan.cpp).
 //  Phase 1 (blocks >= 256 entries, buckets >= 9): multi-warp groups (16/8/4/2 warps for
@@ -77,9 +80,29 @@ __device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Streaming variant: the tile arrays are read once per pass, so they are loaded with an L2 evict-first
+// policy and do not push the CTA accumulator copies, tile descriptors and duals out of L2.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                    uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void red_add_f64(double* a, double v) {  // fire-and-forget fp64 reduction
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -184,10 +207,13 @@ template <int M, int LM, bool WX>
 struct Ctx {
   const GradArgs& p;
   const float* lam_s;  // duals staged in shared memory (LM != kLamGlobal)
+  double* acc;         // this CTA's accumulator copy
   double gamma, invgamma;
   double cx = 0.0, reg = 0.0;
   float nx = 0.f;
-  __device__ Ctx(const GradArgs& pp, const float* ls, double g) : p(pp), lam_s(ls), gamma(g), invgamma(1.0 / g) {}
+  __device__ Ctx(const GradArgs& pp, const float* ls, double g)
+      : p(pp), lam_s(ls), acc(pp.acc + (size_t)(blockIdx.x % pp.acc_copies) * pp.acc_stride), gamma(g),
+        invgamma(1.0 / g) {}
 
   // dual of family f at destination label j: shared memory (all, or the hot labels [0, H) of
   // the popularity order, R15) or global memory (L2-resident m*J floats)
@@ -202,7 +228,7 @@ struct Ctx {
   // contribution of one positive x (fp64) to A x, the objective scalars and x_out
   __device__ __forceinline__ void emit(int j, float cval, const float* av, double x, double vs, int b, int e) {
 #pragma unroll
-    for (int f = 0; f < M; ++f) red_add_f64(p.acc + (size_t)f * p.J + j, (double)av[f] * x);
+    for (int f = 0; f < M; ++f) red_add_f64(acc + (size_t)f * p.J + j, (double)av[f] * x);
     cx += (double)cval * x;
     reg += 0.5 * gamma * vs * x * x;
     nx += 1.f;
@@ -1337,6 +1363,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   extern __shared__ __align__(128) char smem[];
   SmemHead* head = reinterpret_cast<SmemHead*>(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned long long* trace = p.trace ? p.trace + 5 * blockIdx.x : nullptr;
+  if (trace && threadIdx.x == 0) {
+    uint32_t sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    trace[0] = sm;
+    trace[1] = globaltimer();
+    trace[4] = 0;  // tile count, added by every warp after the barrier below
+  }
   char* after_head = smem + 2048;
   float* lam_s = nullptr;
   size_t lam_bytes = 0;
@@ -1356,9 +1390,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   for (int i = threadIdx.x; i <= kRcpN; i += kThreads) head->rcp[i] = c_rcp[i];
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  if (trace && threadIdx.x == 0) trace[2] = globaltimer();
 
   const double gamma = p.gamma_ptr ? *p.gamma_ptr : p.gamma_val;
   Ctx<M, LM, WX> C(p, lam_s, gamma);
+  unsigned ntiles = 0;  // tiles this warp worked (trace only)
 
   // ---- phase 1: big blocks, groups of 16 / 8 / 4 / 2 warps; barrier ids unique per group
   for (int ph = 0; ph < kNumBigPhases; ++ph) {
@@ -1382,6 +1418,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       const int ti = head->slot[g.bar];
       if (ti >= p.ph_begin[ph + 1]) break;
       const Tile tl = p.tiles[ti];
+      ntiles += g.gtid == 0;
       double* scr = tl.nnz <= scr_cap ? scr_smem : p.gscratch + (size_t)blockIdx.x * p.gscratch_per_cta;
       if constexpr (KIND == DL_PROJ_SIMPLEX)
         big_block_simplex<M, LM, WX>(C, g, tl, scr_smem, scr_cap, scr);
@@ -1435,11 +1472,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
         char* dst = mybuf + (size_t)st * stage_bytes;
         fence_proxy_async();
         mbar_expect_tx(&bars[st], bytes * (2u + M) + rbytes);
-        tma_bulk_g2s(dst, p.dest + t.off, bytes, &bars[st]);
-        tma_bulk_g2s(dst + (size_t)p.tile_cap * 4, p.c + t.off, bytes, &bars[st]);
+        const uint64_t pol = evict_first_policy();
+        tma_bulk_g2s_stream(dst, p.dest + t.off, bytes, &bars[st], pol);
+        tma_bulk_g2s_stream(dst + (size_t)p.tile_cap * 4, p.c + t.off, bytes, &bars[st], pol);
 #pragma unroll
         for (int f = 0; f < M; ++f)
-          tma_bulk_g2s(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st]);
+          tma_bulk_g2s_stream(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st],
+                              pol);
         if (rbytes) tma_bulk_g2s(meta + 256 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
       }
     };
@@ -1484,9 +1523,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
         small_dispatch<M, LM, WX, true>(C, t, mybuf + (size_t)st * stage_bytes, lane, rslot + st * 64, cslot,
                                         head->rcp);
       __syncwarp();
+      ++ntiles;
       if (same) {
         ++pos;
       } else {  // chunk c0 done: its descriptor slot takes chunk c2
+        if (trace && lane == 0) p.trace[5 * gridDim.x + (c0 - s_begin) / kChunk] = globaltimer();
         const int c2 = first_of(c2raw);
         __syncwarp();
         issue_desc(c2, ds);
@@ -1512,9 +1553,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   }
   if (lane == 0) {
     const size_t n = (size_t)M * p.J;
-    atomicAdd(p.acc + n + 0, cx);
-    atomicAdd(p.acc + n + 1, rg);
-    atomicAdd(p.acc + n + 2, (double)nx);
+    atomicAdd(C.acc + n + 0, cx);
+    atomicAdd(C.acc + n + 1, rg);
+    atomicAdd(C.acc + n + 2, (double)nx);
+    if (trace) atomicAdd(trace + 4, (unsigned long long)ntiles);
+  }
+  if (trace) {
+    __syncthreads();
+    if (threadIdx.x == 0) trace[3] = globaltimer();
   }
 }
 

@@ -115,11 +115,15 @@ struct GradArgs {
   double r, u;             // polytope caps (inf where absent)
   int32_t kind;
   int32_t tile_cap;
-  double* acc;             // [m*J + 4], rows by label
+  double* acc;             // per-CTA partial accumulators: copy (blockIdx % acc_copies) at acc + copy * acc_stride,
+                           // rows [m*J + 4] by label (summed by launch_partial_sum)
+  int64_t acc_stride;
+  int32_t acc_copies;
   int32_t* ctr;            // [8] work-queue counters (zeroed before launch)
   float* x_out;            // primal output (original order) or nullptr
   double* gscratch;        // global fp64 d-scratch for blocks beyond the smem scratch
   int64_t gscratch_per_cta;
+  unsigned long long* trace;  // per CTA {smid, t_start, t_staged, t_end, tiles} (dl_debug_trace) or nullptr
 };
 
 cudaError_t launch_fused_grad(const GradArgs& a, int ctas, size_t smem, cudaStream_t s);
@@ -143,6 +147,9 @@ struct StepArgs {
   double* scal;            // [2] eta, beta of the step
 };
 cudaError_t launch_agd_step(const StepArgs& a, cudaStream_t s);
+// acc[r] = sum over copies c (in order) of part[c * stride + r] for r < n, and part[c * stride + r] = 0
+// (the per-CTA partials of the fused pass -> the accumulator; deterministic order)
+cudaError_t launch_partial_sum(double* part, int64_t stride, int32_t copies, int64_t n, double* acc, cudaStream_t s);
 
 struct FinalizeArgs {
   int32_t n, J;

@@ -139,12 +139,8 @@ __global__ void __launch_bounds__(kRedThreads) agd_update_kernel(const StepArgs 
     a.lam1[r] = l1n;
     a.lam2[r] = l2n;
     a.mu[r] = (float)(a.D[r] * l2n);
-    a.acc[r] = 0.0;
   }
-  if (blockIdx.x == 0) {
-    if (threadIdx.x < 4) a.acc[n + threadIdx.x] = 0.0;
-    if (threadIdx.x < 8) a.ctr[threadIdx.x] = 0;
-  }
+  if (blockIdx.x == 0 && threadIdx.x < 8) a.ctr[threadIdx.x] = 0;
 }
 
 // grad = A x - b (or A x if partial), un-permuted to ORIGINAL order; obj = {g, c^T x, reg, nnz(x)}.
@@ -278,6 +274,47 @@ cudaError_t launch_agd_step(const StepArgs& a, cudaStream_t s) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   agd_update_kernel<<<std::max(1, std::min(4 * 148, (a.n + kRedThreads - 1) / kRedThreads)), kRedThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+// 32 rows x 8 copy groups per CTA: warp w sums copies w, w + 8, ... of row (CTA base + lane) in
+// order, warp 0 adds the 8 group sums in order; every copy row read is zeroed for the next pass.
+// Loads are issued kB at a time before any store (the zeroing stores would otherwise serialise them).
+__global__ void __launch_bounds__(256) partial_sum_kernel(double* part, int64_t stride, int32_t copies, int64_t n,
+                                                          double* acc) {
+  constexpr int kB = 10;
+  __shared__ double sm[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * 32 + lane;
+  double v = 0.0;
+  if (r < n) {
+    for (int c0 = w; c0 < copies; c0 += 8 * kB) {
+      double t[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int c = c0 + 8 * k;
+        t[k] = c < copies ? __ldcg(part + (size_t)c * stride + r) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int c = c0 + 8 * k;
+        v += t[k];
+        if (c < copies) part[(size_t)c * stride + r] = 0.0;
+      }
+    }
+  }
+  sm[w][lane] = v;
+  __syncthreads();
+  if (w == 0 && r < n) {
+    double t = sm[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += sm[k][lane];
+    acc[r] = t;
+  }
+}
+
+cudaError_t launch_partial_sum(double* part, int64_t stride, int32_t copies, int64_t n, double* acc, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  partial_sum_kernel<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(part, stride, copies, n, acc);
   return cudaGetLastError();
 }
 cudaError_t launch_finalize(const FinalizeArgs& a, cudaStream_t s) {
