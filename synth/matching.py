@@ -24,8 +24,9 @@ full-row-rank assumption of PAPER.md:229).
 from __future__ import annotations
 
 import dataclasses
+import mmap
 import multiprocessing as mp
-from concurrent.futures import ProcessPoolExecutor, ThreadPoolExecutor
+from concurrent.futures import ProcessPoolExecutor
 
 import numpy as np
 
@@ -186,51 +187,90 @@ def _gen_chunk(cfg: GenConfig, dp: dict, chunk_id: int):
 _DP_CACHE: dict = {}
 
 
-def _gen_chunk_job(args):
-    """Process-pool worker: one chunk (dest_params cached per process)."""
-    cfg, cid = args
+_SH: dict = {}  # the shard's output arrays (anonymous shared memory, inherited by forked workers)
+
+
+def _raw_degrees(cfg: GenConfig, chunk_id: int) -> np.ndarray:
+    """The chunk's degree draw (the first draw of its stream, as in _gen_chunk): an upper bound of
+    every source's final length (duplicate destinations are merged afterwards)."""
+    nsrc = min(cfg.chunk, cfg.num_sources - chunk_id * cfg.chunk)
+    g = _rng(cfg.seed, 2, chunk_id)
+    if cfg.length_law == "poisson":
+        deg = g.poisson(cfg.nnz_per_source, size=nsrc)
+    else:
+        deg = np.searchsorted(_powerlaw_cdf(cfg), g.random(nsrc), side="right") + 1
+    return np.minimum(deg, cfg.num_dests).astype(np.int64)
+
+
+def _shared(shape, dtype):
+    n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    buf = mmap.mmap(-1, max(n, 1))
+    return np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+
+def _shard_job(args):
+    """One chunk's slice [lo, hi) written into the shared arrays at edge offset e_raw / source
+    offset s_off; returns (edges written, greedy-load partial)."""
+    cfg, cid, lo, hi, e_raw, s_off = args
     dp = _DP_CACHE.get(cfg)
     if dp is None:
         dp = _DP_CACHE[cfg] = dest_params(cfg)
-    return _gen_chunk(cfg, dp, cid)
+    lens, dest, c, a, ld = _gen_chunk(cfg, dp, cid)
+    e0, e1 = int(lens[:lo].sum()), int(lens[:hi].sum())
+    if lo != 0 or hi != lens.size:  # partial chunk: the greedy load of the kept sources only
+        ld = _greedy_load(lens[lo:hi], dest[e0:e1], a[:, e0:e1], cfg.num_dests)
+    n = e1 - e0
+    _SH["lens"][s_off:s_off + hi - lo] = lens[lo:hi]
+    _SH["dest"][e_raw:e_raw + n] = dest[e0:e1]
+    _SH["c"][e_raw:e_raw + n] = c[e0:e1]
+    _SH["a"][:, e_raw:e_raw + n] = a[:, e0:e1]
+    return n, ld
 
 
 def generate_shard(cfg: GenConfig, src_begin: int, src_end: int, threads: int = 8):
     """Sources [src_begin, src_end) of the instance, plus their greedy-load partial.
 
     Returns (Instance with b=None, partial_load[m, J] float64).  The full b needs
-    the sum of partial loads over all shards (``capacities``).
+    the sum of partial loads over all shards (``capacities``).  Chunks are generated by forked
+    worker processes straight into shared output arrays sized by the chunks' degree draws (an upper
+    bound), then compacted in place: peak memory is about one copy of the shard.
     """
-    dp = dest_params(cfg)
+    m, J = cfg.num_families, cfg.num_dests
     c0, c1 = src_begin // cfg.chunk, (max(src_end, src_begin + 1) - 1) // cfg.chunk
     ids = list(range(c0, c1 + 1)) if src_end > src_begin else []
-    if threads > 1 and len(ids) >= 4 * threads:  # many chunks: forked worker processes (numpy holds the GIL)
-        with ProcessPoolExecutor(max_workers=threads, mp_context=mp.get_context("fork")) as ex:
-            parts = list(ex.map(_gen_chunk_job, [(cfg, cid) for cid in ids], chunksize=1))
-    else:
-        with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
-            parts = list(ex.map(lambda cid: _gen_chunk(cfg, dp, cid), ids))
-    lens_l, dest_l, c_l, a_l = [], [], [], []
-    load = np.zeros((cfg.num_families, cfg.num_dests), dtype=np.float64)
-    for cid, (lens, dest, c, a, ld) in zip(ids, parts):
+    jobs, e_raw, s_off = [], 0, 0
+    for cid in ids:
         i0 = cid * cfg.chunk
-        lo, hi = max(src_begin, i0) - i0, min(src_end, i0 + lens.size) - i0
-        e0, e1 = int(lens[:lo].sum()), int(lens[:hi].sum())
-        lens_l.append(lens[lo:hi]); dest_l.append(dest[e0:e1]); c_l.append(c[e0:e1]); a_l.append(a[:, e0:e1])
-        if lo == 0 and hi == lens.size:
-            load += ld
-        else:  # partial chunk: recompute the greedy load of the kept sources only
-            load += _greedy_load(lens[lo:hi], dest[e0:e1], a[:, e0:e1], cfg.num_dests)
-    lens = np.concatenate(lens_l) if lens_l else np.zeros(0, np.int64)
+        nsrc = min(cfg.chunk, cfg.num_sources - i0)
+        lo, hi = max(src_begin, i0) - i0, min(src_end, i0 + nsrc) - i0
+        jobs.append((cfg, cid, lo, hi, e_raw, s_off))
+        e_raw += int(_raw_degrees(cfg, cid)[lo:hi].sum())
+        s_off += hi - lo
+    _SH["lens"] = _shared((s_off,), np.int64)
+    _SH["dest"] = _shared((e_raw,), np.int32)
+    _SH["c"] = _shared((e_raw,), np.float32)
+    _SH["a"] = _shared((m, e_raw), np.float32)
+    if threads > 1 and len(ids) >= 2 * threads:  # forked workers (numpy holds the GIL) write in place
+        with ProcessPoolExecutor(max_workers=threads, mp_context=mp.get_context("fork")) as ex:
+            res = list(ex.map(_shard_job, jobs, chunksize=1))
+    else:
+        res = [_shard_job(j) for j in jobs]
+    load = np.zeros((m, J), dtype=np.float64)
+    nnz = 0
+    for (cfg_, cid, lo, hi, raw, so), (n, ld) in zip(jobs, res):  # compaction, left to right (nnz <= raw)
+        if raw != nnz:
+            _SH["dest"][nnz:nnz + n] = _SH["dest"][raw:raw + n]
+            _SH["c"][nnz:nnz + n] = _SH["c"][raw:raw + n]
+            _SH["a"][:, nnz:nnz + n] = _SH["a"][:, raw:raw + n]
+        nnz += n
+        load += ld
+    lens = _SH.pop("lens")
+    dest, c, a = _SH.pop("dest")[:nnz], _SH.pop("c")[:nnz], _SH.pop("a")
+    a = a[:, :nnz] if m == 1 else np.ascontiguousarray(a[:, :nnz])
     row_ptr = np.zeros(lens.size + 1, dtype=np.int64)
     np.cumsum(lens, out=row_ptr[1:])
-    m = cfg.num_families
-    inst = Instance(num_sources=int(lens.size), num_dests=cfg.num_dests, num_families=m,
-                    row_ptr=row_ptr,
-                    dest=np.concatenate(dest_l) if dest_l else np.zeros(0, np.int32),
-                    a=np.concatenate(a_l, axis=1) if a_l else np.zeros((m, 0), np.float32),
-                    c=np.concatenate(c_l) if c_l else np.zeros(0, np.float32),
-                    b=None, source_offset=src_begin)
+    inst = Instance(num_sources=int(lens.size), num_dests=J, num_families=m, row_ptr=row_ptr,
+                    dest=dest, a=a, c=c, b=None, source_offset=src_begin)
     return inst, load
 
 
