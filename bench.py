@@ -61,6 +61,10 @@ def parse():
     return ap.parse_args()
 
 
+def log(msg):
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -228,7 +232,11 @@ def main():
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     cfg_idx, kind, proj_r, proj_u, proj_desc = WORKLOADS[args.config]
+    log(f"generated {inst.nnz} nnz in {t_gen:.1f} s")
+    t_create = time.perf_counter()
     gp = MatchingProblem.from_instance(inst, kind=kind, r=proj_r, u=proj_u, device=local, stream=stream)
+    t_create = time.perf_counter() - t_create
+    log(f"created in {t_create:.1f} s: {gp.info}")
     if world > 1:
         gp.comm_init(rank, world)
     rowsq = gp.row_sqnorms()
