@@ -2,18 +2,27 @@
 """Benchmark of the dual-gradient hot path (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--config NAME]
+                    [--scaling weak|strong] [--comm] [--no-gap] [--no-cpu]
 
-A step is one iteration of the whole hot path (DESIGN.md §8(a) A3-A5): the fused
-dual-gradient pass over every edge of the instance, the gradient all-reduce
-(N > 1), and the on-device AGD step.  `value` = edges processed by all ranks per
-second of device time (max over ranks), i.e. nnz/s per dual-gradient evaluation.
-Extra keys: roofline of the fused kernel, the oracle CPU baseline, end-to-end
-throughput through the host-buffer C-ABI entry, and time to a 1e-3 relative dual
-gap (R11).
+A step is one iteration of the whole hot path (DESIGN.md §8(a) A3-A5): the fused dual-gradient
+pass over every edge of the instance (+ the sum of its per-CTA accumulator copies), the gradient
+all-reduce (N > 1, or --comm at N = 1: the same NCCL path with one rank), and the on-device AGD
+step.  `value` = edges processed by all ranks per second of device time (max over ranks), i.e.
+nnz/s per dual-gradient evaluation.  Default workload: BASELINE configs[2] (100M sources x 100k
+destinations, 5e9 nnz, the configuration the metric's 1/2/4/8-GPU numbers are quoted on).
 
-N > 1 (torchrun): weak scaling -- rank r owns sources [r I, (r+1) I) of an
-instance with N I sources generated shard-locally (synth, Philox chunks); lambda
-is replicated and one NCCL all-reduce of the m J + 4 accumulator runs per step.
+Order: (1) time to a 1e-3 relative dual gap (R11): the solver runs from iteration 0 in
+graph-captured chunks of 8 iterations with a CUDA event after each chunk until the best dual value
+is settled (>= 2 t* iterations and < 1e-5 relative improvement over the second half, or 4 t*);
+(2) W warm-up + K timed steps at the state reached, CUDA events around every step and around every
+fused-pass launch (dl_set_pass_events: the roofline kernel time); (3) end to end through the
+host-buffer C-ABI entry; (4) the oracle on the host cores.
+
+Multi-GPU: weak scaling -- rank r owns sources [r I, (r+1) I) of an instance with N I sources --
+or strong scaling -- the instance of the workload split into N contiguous source ranges; the
+default is strong for the 5e9 / 2e9-nnz workloads (their host-side generation would not fit N
+copies) and weak otherwise.  Shards are generated rank-locally (Philox chunks), lambda is
+replicated and one NCCL all-reduce of the m J + 4 accumulator runs per step.
 """
 from __future__ import annotations
 
@@ -30,15 +39,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WORKLOAD = "1M_x_10k"           # BASELINE.json configs[1]: 1M x 10k, ~100 nnz/source, simplex, Jacobi, 1 B200
-# workload -> (BASELINE.json configs index, projection kind, r, u, description); kinds as in include/dualip.h
+WORKLOAD = "100M_x_100k"        # BASELINE.json configs[2]: 100M x 100k, ~50 nnz/source (5e9 nnz), simplex
+# workload -> (BASELINE.json configs index, projection kind, r, u, description, default scaling)
 WORKLOADS = {
-    "tiny": (0, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
-    "1M_x_10k": (1, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
-    "100M_x_100k": (2, 0, 1.0, 1.0, "simplex (sum x <= 1)"),
-    "multifamily_boxcut": (3, 1, 3.0, 1.0, "box-cut (0 <= x <= 1, sum x <= 3), 2 families (capacity + budget)"),
-    "powerlaw": (4, 0, 1.0, 1.0, "simplex (sum x <= 1), power-law block lengths 1..10k"),
-    "paper_table_25M": (None, 0, 1.0, 1.0, "simplex (sum x <= 1), the paper's timing-table instance"),
+    "tiny": (0, 0, 1.0, 1.0, "simplex (sum x <= 1)", "weak"),
+    "1M_x_10k": (1, 0, 1.0, 1.0, "simplex (sum x <= 1)", "weak"),
+    "100M_x_100k": (2, 0, 1.0, 1.0, "simplex (sum x <= 1)", "strong"),
+    "multifamily_boxcut": (3, 1, 3.0, 1.0, "box-cut (0 <= x <= 1, sum x <= 3), 2 families (capacity + budget)",
+                           "weak"),
+    "powerlaw": (4, 0, 1.0, 1.0, "simplex (sum x <= 1), power-law block lengths 1..10k", "strong"),
+    "paper_table_25M": (None, 0, 1.0, 1.0, "simplex (sum x <= 1), the paper's timing-table instance", "weak"),
 }
 # The paper's own numbers, another machine's (context, not the target; BASELINE.json publishes none)
 PAPER_CONTEXT = ("PAPER.md:455-476 (table): average time per AGD iteration at 25M sources x 10k destinations, "
@@ -46,19 +56,27 @@ PAPER_CONTEXT = ("PAPER.md:455-476 (table): average time per AGD iteration at 25
                  "2.46 s; PAPER.md:18 claims >= 10x over distributed-CPU DuaLip to a fixed gap. GPU model not "
                  "stated in the text. Same-shape run here: bench.py --config paper_table_25M")
 GAP_TOL = 1e-3
-BURN_ITERS = 2500                # solver iterations before the timed steps (~ the 1e-3 gap point)
+GAP_SETTLE = 1e-5                # reference run ends when its best value moved < this (relative) over its 2nd half
+GAP_MAX_ITERS = 20000
+SCHEDULE = dict(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3, init_step=1e-5)
+NVLINK_ALLREDUCE_GBS = 725.0     # B200_PROFILING.md: measured 8-rank all-reduce bus bandwidth at 1 GiB
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=WORKLOAD, choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"])
+    ap.add_argument("--comm", action="store_true", help="NCCL communicator and all-reduce also at N = 1")
     ap.add_argument("--no-gap", action="store_true", help="skip the time-to-gap measurement")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle CPU baseline")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.scaling is None:
+        a.scaling = WORKLOADS[a.config][5]
+    return a
 
 
 def log(msg):
@@ -69,88 +87,81 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def shard_config(name, world):
+def shard_range(name, world, rank, scaling):
+    """(full config, first source, end source) of this rank."""
     from synth.matching import CONFIGS
     import dataclasses
     base = CONFIGS[name]
-    return base, dataclasses.replace(base, num_sources=base.num_sources * world)
+    if scaling == "weak":
+        I = base.num_sources
+        return dataclasses.replace(base, num_sources=I * world), rank * I, (rank + 1) * I
+    I = base.num_sources
+    return base, I * rank // world, I * (rank + 1) // world
 
 
 # --------------------------------------------------------------------------- oracle arms
 def oracle_problem(inst, name):
     from oracle.dual import Problem
-    _, kind, r, u, _ = WORKLOADS[name]
+    _, kind, r, u, _, _ = WORKLOADS[name]
     return Problem.from_instance(inst, kind=kind, r=r, u=(np.inf if kind == 0 else u))
 
 
-def oracle_sample(cfg, name, target_s=15.0, max_sources=200_000):
-    """Time oracle.dual_eval on growing prefixes of the workload (same law, same
-    seeds) until ~target_s of CPU work; returns (nnz/s, description)."""
-    import dataclasses
-    from oracle.dual import Problem, dual_eval
-    from synth.matching import generate_shard, capacities
-    n_src = 2000
-    while True:
-        inst, load = generate_shard(cfg, 0, n_src, threads=4)
-        inst.b = capacities(cfg, load * (cfg.num_sources / max(n_src, 1)))
-        P = oracle_problem(inst, name)
-        lam = np.full(P.num_families * P.num_dests, 0.0)
-        t0 = time.process_time()
-        w0 = time.perf_counter()
-        dual_eval(P, lam, 0.01)
-        dt = time.perf_counter() - w0
-        if dt * (target_s / max(dt, 1e-9)) and (dt >= target_s / 4 or n_src >= max_sources):
-            break
-        n_src = min(max_sources, int(n_src * max(2.0, target_s / 4 / max(dt, 1e-3))))
-    reps = max(1, int(target_s / max(dt, 1e-3)))
-    w0 = time.perf_counter()
+def _oracle_part(args):
+    """One worker of the CPU baseline: generate its source range of the sample (same law, same seeds),
+    then time `reps` oracle.dual_eval calls on it."""
+    from oracle.dual import dual_eval
+    from synth.matching import CONFIGS, capacities, generate_shard
+    name, s0, s1, reps = args
+    cfg = CONFIGS[name]
+    inst, load = generate_shard(cfg, s0, s1, threads=1)
+    inst.b = capacities(cfg, load * (cfg.num_sources / max(s1 - s0, 1)))
+    P = oracle_problem(inst, name)
+    lam = np.zeros(P.num_families * P.num_dests)
+    dual_eval(P, lam, 0.01)
+    t0 = time.perf_counter()
     for _ in range(reps):
         dual_eval(P, lam, 0.01)
-    dt = (time.perf_counter() - w0) / reps
-    return P.nnz / dt, f"oracle.dual.dual_eval (fp64 numpy, per-block sort projection) on the first {n_src} " \
-                       f"sources ({P.nnz} nnz) of {cfg.num_sources}, {reps} reps, {dt:.2f} s/eval"
+    return P.nnz, time.perf_counter() - t0
+
+
+def oracle_cpu(name, target_s=15.0, cores=None):
+    """The fp64 oracle as it stands on `cores` host processes, each on its own contiguous source range
+    of a bounded prefix of the workload (about target_s of wall time); returns (nnz/s, cores, sample)."""
+    import multiprocessing as mp
+    from synth.matching import CONFIGS
+    cfg = CONFIGS[name]
+    cores = cores or max(1, os.cpu_count() or 1)
+    nnz1, dt1 = _oracle_part((name, 0, min(2000, cfg.num_sources), 1))   # probe: seconds per source
+    per_src = dt1 / min(2000, cfg.num_sources)
+    per_core = int(min(cfg.num_sources // cores, max(200, target_s / 3 / max(per_src, 1e-9))))
+    reps = 3
+    jobs = [(name, k * per_core, (k + 1) * per_core, reps) for k in range(cores)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_part, jobs)
+    wall = max(dt for _, dt in res)
+    nnz = sum(n for n, _ in res) * reps
+    sample = (f"oracle.dual.dual_eval (fp64 numpy, per-block sort projection) on {cores} processes, each on "
+              f"{per_core} consecutive sources (first {per_core * cores} of {cfg.num_sources}, "
+              f"{nnz // reps} nnz), {reps} evaluations each at lambda = 0, gamma = 0.01; nnz/s = all "
+              f"evaluated nnz / slowest process time ({wall:.1f} s)")
+    return nnz / wall, cores, sample
 
 
 def run_reference(args):
     """The base contract's reference arm for this tier: the fp64 oracle as it stands, on the host
     cores, each step one dual-gradient evaluation of a bounded prefix of the workload (same law,
-    same seeds), the prefix sized so that warm-up + steps take about two minutes."""
+    same seeds) split over the cores, sized so that warm-up + steps take about two minutes."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle.dual import dual_eval
-    from synth.matching import CONFIGS, capacities, generate_shard
-    cfg = CONFIGS[args.config]
-    budget_s = 120.0 / max(1, args.steps + args.warmup)
-
-    def prefix(n):
-        inst, load = generate_shard(cfg, 0, n, threads=4)
-        inst.b = capacities(cfg, load * (cfg.num_sources / n))
-        return oracle_problem(inst, args.config)
-    n_src = min(500, cfg.num_sources)
-    P = prefix(n_src)
-    lam = np.zeros(P.num_families * P.num_dests)
-    t0 = time.perf_counter()
-    dual_eval(P, lam, 0.01)
-    per_src = (time.perf_counter() - t0) / n_src
-    n_src = int(min(cfg.num_sources, 200_000, max(500, budget_s / max(per_src, 1e-9))))
-    P = prefix(n_src)
-    lam = np.zeros(P.num_families * P.num_dests)
-    for _ in range(args.warmup):
-        dual_eval(P, lam, 0.01)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        dual_eval(P, lam, 0.01)
-    dt = time.perf_counter() - t0
-    v = P.nnz * args.steps / dt
-    sample = (f"oracle.dual.dual_eval (fp64 numpy, 1 thread) on the first {n_src} sources ({P.nnz} nnz) "
-              f"of {args.config}, lambda = 0, gamma = 0.01")
+    v, cores, sample = oracle_cpu(args.config, target_s=120.0 / max(1, (args.steps + args.warmup) / 5))
     print(json.dumps({
         "impl": "reference", "metric": "nnz/s per dual-gradient eval", "value": v, "unit": "nnz/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "sample": sample},
-        "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "nnz/s", "cores": cores, "kind": "oracle", "sample": sample},
         "e2e": {"value": v, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -218,27 +229,27 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    base, full = shard_config(args.config, world)
-    I = base.num_sources
+    full, s0, s1 = shard_range(args.config, world, rank, args.scaling)
     threads = max(1, (os.cpu_count() or 8) // world)
     t_gen = time.perf_counter()
-    inst, load = generate_shard(full, rank * I, (rank + 1) * I, threads=threads)
+    inst, load = generate_shard(full, s0, s1, threads=threads)
     load_t = torch.from_numpy(load).to(dev)
     if world > 1:
         dist.all_reduce(load_t)
     inst.b = capacities(full, load_t.cpu().numpy())
     t_gen = time.perf_counter() - t_gen
+    log(f"rank {rank}: generated sources [{s0}, {s1}) ({inst.nnz} nnz) in {t_gen:.1f} s")
 
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    cfg_idx, kind, proj_r, proj_u, proj_desc = WORKLOADS[args.config]
-    log(f"generated {inst.nnz} nnz in {t_gen:.1f} s")
+    cfg_idx, kind, proj_r, proj_u, proj_desc, _ = WORKLOADS[args.config]
     t_create = time.perf_counter()
     gp = MatchingProblem.from_instance(inst, kind=kind, r=proj_r, u=proj_u, device=local, stream=stream)
+    use_comm = world > 1 or args.comm
+    if use_comm:
+        gp.comm_init(rank, world)
     t_create = time.perf_counter() - t_create
     log(f"created in {t_create:.1f} s: {gp.info}")
-    if world > 1:
-        gp.comm_init(rank, world)
     rowsq = gp.row_sqnorms()
     gp.allreduce(rowsq)
     gp.set_jacobi(rowsq)
@@ -249,52 +260,104 @@ def main():
     nnz_total = float(nnz_t.item())
     m = inst.num_families
     algo_bytes = nnz_local * (8 + 4 * m)
-
-    # ---- timed region: K hot-path steps (eval -> [all-reduce] -> step), events around each fused launch
     acc_ptr, acc_n = L.dl_agd_accumulator(gp.h)
-    gp.agd_init(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3, init_step=1e-5)
+    del inst
 
-    def one_step(ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        L.dl_agd_eval(gp.h)
-        if ev is not None:
-            ev[1].record(stream)
+    def sync_all():
+        stream.synchronize()
         if world > 1:
-            L.dl_comm_allreduce(gp.h, acc_ptr, acc_n)
-        L.dl_dual_step(gp.h)
+            dist.barrier()
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)  # creates the event handle (the C-ABI records it again where it is used)
+        return e
 
     with ClockSampler(local) as clk:
-        # burn-in: the solver runs to iteration BURN_ITERS (the regime of the time-to-gap run,
-        # deterministic state; ~1 s of load, clocks steady), then W warm-up steps of the timed loop
-        gp.solve(BURN_ITERS)
-        for _ in range(args.warmup):
-            one_step()
-        stream.synchronize()
-        if world > 1:
-            dist.barrier()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # ---- (1) time to a 1e-3 relative dual gap, from iteration 0 (R11)
+        gap = None
+        gp.agd_init(history_cap=GAP_MAX_ITERS + 64, **SCHEDULE)
+        gp.solve(8)  # graph instantiation outside the timed run
+        gp.agd_init(history_cap=GAP_MAX_ITERS + 64, **SCHEDULE)
+        sync_all()
+        if not args.no_gap:
+            chunk_ev = [ev()]
+            it, t_star, ghat = 0, None, None
+            while it < GAP_MAX_ITERS:
+                n = 8 * 32
+                for _ in range(32):
+                    gp.solve(8)
+                    chunk_ev.append(ev())
+                it += n
+                g = gp.history()["g"]
+                best = np.maximum.accumulate(g)
+                ghat = float(best[-1])
+                hit = np.flatnonzero(ghat - best <= GAP_TOL * abs(ghat))
+                t_star = int(hit[0]) + 1 if hit.size else None
+                if t_star is None:
+                    continue
+                settled = it >= 2 * t_star and (best[-1] - best[it // 2 - 1]) <= GAP_SETTLE * abs(ghat)
+                if settled or it >= 4 * t_star:
+                    break
+            stream.synchronize()
+            if t_star is not None:
+                k = (t_star + 7) // 8            # chunks up to the one that reaches the gap
+                tg = torch.tensor([chunk_ev[0].elapsed_time(chunk_ev[k])], dtype=torch.float64, device=dev)
+                if world > 1:
+                    dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+                gap = {"iterations": t_star, "seconds": float(tg.item()) / 1e3, "rel_gap": GAP_TOL, "g_hat": ghat,
+                       "reference_iters": it,
+                       "reference_rule": f">= 2 t* with < {GAP_SETTLE:g} relative gain over its second half, "
+                                         f"or 4 t*",
+                       "timed": "solver from iteration 0 (graph chunks of 8), events per chunk; up to the end "
+                                "of the chunk containing t*",
+                       "schedule": "gamma 0.16 -> 0.01 halved every 25, max_step 1e-3 at gamma 0.01, Jacobi"}
+            else:
+                gap = {"iterations": None, "seconds": None, "rel_gap": GAP_TOL, "reference_iters": it}
+            log(f"time to gap: {gap}")
+        else:
+            gp.solve(2496)
+        t_from = int(gp.history()["iter"][-1]) + 1 if len(gp.history()) else 0
+
+        # ---- (2) W warm-up + K timed steps: eval (fused pass + copy sum) -> [all-reduce] -> step
+        evs = [(ev(), ev(), ev(), ev(), ev(), ev()) for _ in range(args.warmup + args.steps)]
+
+        def one_step(e):
+            e[0].record(stream)
+            L.dl_set_pass_events(gp.h, e[1], e[2])
+            L.dl_agd_eval(gp.h)
+            e[3].record(stream)
+            if use_comm:
+                L.dl_comm_allreduce(gp.h, acc_ptr, acc_n)
+            e[4].record(stream)
+            L.dl_dual_step(gp.h)
+            e[5].record(stream)
+        for k in range(args.warmup):
+            one_step(evs[k])
+        sync_all()
+        t0, t1 = ev(), ev()
         t0.record(stream)
-        for k in range(args.steps):
+        for k in range(args.warmup, args.warmup + args.steps):
             one_step(evs[k])
         t1.record(stream)
-        stream.synchronize()
-        if world > 1:
-            dist.barrier()
+        sync_all()
+        L.dl_set_pass_events(gp.h)
+    timed = evs[args.warmup:]
     ms_total = t0.elapsed_time(t1)
-    kern_ms = [a.elapsed_time(b) for a, b in evs]
-    ms_t = torch.tensor([ms_total, float(np.mean(kern_ms))], dtype=torch.float64, device=dev)
+    kern = np.mean([e[1].elapsed_time(e[2]) for e in timed])
+    evalms = np.mean([e[0].elapsed_time(e[3]) for e in timed])
+    arms = np.mean([e[3].elapsed_time(e[4]) for e in timed])
+    stepms = np.mean([e[4].elapsed_time(e[5]) for e in timed])
+    ms_t = torch.tensor([ms_total, kern, evalms, arms, stepms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_total, kern_avg = float(ms_t[0]), float(ms_t[1])
+    ms_total, kern, evalms, arms, stepms = (float(x) for x in ms_t)
     value = nnz_total * args.steps / (ms_total / 1e3)
+    log(f"steps: {ms_total / args.steps:.3f} ms/step, fused {kern:.3f} ms, eval {evalms:.3f}, all-reduce {arms:.3f}")
 
-    # ---- end to end through the host-buffer entry (pinned host lambda in, gradient + objective out)
+    # ---- (3) end to end through the host-buffer entry (pinned host lambda in, gradient + objective out)
     n = gp.n
-    _, l2_now = gp.dual()  # the dual point the timed steps were at
-    lam_h = torch.from_numpy(l2_now.astype(np.float32)).pin_memory()
+    lam_h = torch.from_numpy(gp.point()).pin_memory()
     grad_h = torch.zeros(n, dtype=torch.float64).pin_memory()
     obj_h = torch.zeros(4, dtype=torch.float64).pin_memory()
     grad_d, obj_d = gp.new_grad_buffers()
@@ -303,14 +366,14 @@ def main():
     def e2e_step():
         if world == 1:
             gp.dual_grad_host(lam_h, 0.01, grad_h, obj_h)
-        else:  # same public calls composed: H2D, partial gradient, all-reduce, D2H
+        else:  # the same public calls composed: H2D, partial gradient, all-reduce, D2H
             lam_d.copy_(lam_h, non_blocking=True)
             L.dl_dual_grad(gp.h, L.ptr(lam_d), 0.01, L.ptr(grad_d), L.ptr(obj_d), L.DL_GRAD_PARTIAL)
             L.dl_comm_allreduce(gp.h, L.ptr(grad_d), n)
             grad_h.copy_(grad_d, non_blocking=True)
             obj_h.copy_(obj_d, non_blocking=True)
             stream.synchronize()
-    for _ in range(3):
+    for _ in range(2):
         e2e_step()
     if world > 1:
         dist.barrier()
@@ -322,41 +385,6 @@ def main():
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = nnz_total * args.steps / float(e2e_t.item())
-
-    # ---- time to a 1e-3 relative dual gap (continuation 0.16 -> 0.01, Jacobi; R11)
-    gap = None
-    if not args.no_gap:
-        ref_iters = 8000
-        gp.agd_init(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3, init_step=1e-5,
-                    history_cap=ref_iters)
-        gp.solve(ref_iters)
-        h = gp.history()
-        ghat = float(np.max(h["g"]))
-        best = np.maximum.accumulate(h["g"])
-        hit = np.flatnonzero(ghat - best <= GAP_TOL * abs(ghat))
-        t_star = int(hit[0]) + 1 if hit.size else None
-        if t_star is not None:
-            gp.agd_init(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3,
-                        init_step=1e-5, history_cap=ref_iters)
-            gp.solve(16)  # graph instantiation outside the timed region
-            gp.agd_init(gamma0=0.16, gamma_min=0.01, halve_every=25, use_jacobi=True, max_step=1e-3,
-                        init_step=1e-5, history_cap=ref_iters)
-            stream.synchronize()
-            if world > 1:
-                dist.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            gp.solve(t_star)
-            b.record(stream)
-            stream.synchronize()
-            tg = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-            gap = {"iterations": t_star, "seconds": float(tg.item()) / 1e3, "rel_gap": GAP_TOL,
-                   "g_hat": ghat, "reference_iters": ref_iters,
-                   "schedule": "gamma 0.16 -> 0.01 halved every 25, max_step 1e-3 at gamma 0.01, Jacobi"}
-        else:
-            gap = {"iterations": None, "seconds": None, "rel_gap": GAP_TOL, "reference_iters": ref_iters}
 
     if rank == 0:
         peaks = {}
@@ -372,41 +400,58 @@ def main():
                 traffic = prof.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             pass
-        achieved = algo_bytes / (kern_avg / 1e3) / 1e9
+        achieved = algo_bytes / (kern / 1e3) / 1e9
         cpu = None
         if world == 1 and not args.no_cpu:
-            v, sample = oracle_sample(base, args.config)
-            cpu = {"value": v, "unit": "nnz/s", "cores": 1, "kind": "oracle", "sample": sample}
+            v, cores, sample = oracle_cpu(args.config)
+            cpu = {"value": v, "unit": "nnz/s", "cores": cores, "kind": "oracle", "sample": sample}
+        ar = None
+        if use_comm:
+            nbytes = 8 * acc_n
+            bus = (2 * (world - 1) / world * nbytes / (arms / 1e3) / 1e9) if world > 1 else 0.0
+            ar = {"bytes_per_step": nbytes, "ms": arms, "bus_gbs": bus, "peak_gbs": NVLINK_ALLREDUCE_GBS,
+                  "frac": bus / NVLINK_ALLREDUCE_GBS, "peak_source": "B200_PROFILING.md measured 8-rank "
+                  "all-reduce bus bandwidth (1 GiB); at N = 1 the one-rank all-reduce moves no data"}
         out = {
             "metric": "nnz/s per dual-gradient eval", "value": value, "unit": "nnz/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 data, f64 scores/accum",
-            "data": "synthetic",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": "f32 data, f64 scores/accum", "data": "synthetic",
             "config": {"workload": (f"{args.config} (BASELINE configs[{cfg_idx}])" if cfg_idx is not None
                                     else f"{args.config} (PAPER.md:455-476 table instance)"),
-                       "num_sources_per_gpu": I,
-                       "num_dests": base.num_dests, "families": m, "nnz_total": int(nnz_total),
+                       "num_sources": full.num_sources if args.scaling == "strong" else full.num_sources,
+                       "num_sources_per_gpu": s1 - s0,
+                       "num_dests": full.num_dests, "families": m, "nnz_total": int(nnz_total),
                        "projection": proj_desc, "jacobi": True,
                        "l2": (f"inputs ({8 + 4 * m} B/nnz, {algo_bytes / 1e9:.2f} GB per GPU) exceed the 126 MB L2; "
                               "no flush needed" if algo_bytes > 4 * 126e6 else
                               f"inputs ({algo_bytes / 1e6:.0f} MB) are L2-resident: not a bench workload"),
-                       "parallelism": f"dp{world} (sources sharded, lambda replicated, 1 NCCL all-reduce/step)",
-                       "step": "fused dual-gradient pass + all-reduce + on-device AGD step",
-                       "timed_from_iteration": BURN_ITERS + args.warmup},
+                       "parallelism": (f"dp{world} ({args.scaling} scaling: sources sharded, lambda replicated, "
+                                       f"1 NCCL all-reduce of m J + 4 fp64 per step)" if use_comm else
+                                       "dp1 (one GPU, no communicator)"),
+                       "step": "fused dual-gradient pass + CTA-copy sum + [all-reduce] + on-device AGD step",
+                       "timed_from_iteration": t_from + args.warmup},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "fused_grad_kernel", "kernel_ms": kern_avg,
+                         "kernel": "fused_grad_kernel", "kernel_ms": kern,
+                         "kernel_share_of_step": kern / (ms_total / args.steps),
                          "algorithmic_bytes_per_launch": algo_bytes,
+                         "timing": "CUDA events recorded by the C ABI immediately around each fused launch "
+                                   "(dl_set_pass_events), mean of the timed steps, max over ranks",
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+            "step_breakdown_ms": {"fused_pass": kern, "eval_incl_copy_sum": evalms, "allreduce": arms,
+                                  "agd_step": stepms},
+            "allreduce": ar,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "nnz/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 8 * (n + 4)},
-            "gpu_launches": 4 * args.steps,  # per step: fused_grad, deferred, agd_reduce, agd_update kernels
+            "gpu_launches": 4 * args.steps,  # per step: fused_grad, partial_sum, agd_reduce, agd_update
             "clocks": clk.summary(),
             "time_to_gap": gap,
             "paper_context": PAPER_CONTEXT,
-            "setup": {"generate_s": t_gen, "tile_cap": gp.info["tile_cap"], "tiles": gp.info["num_tiles"],
-                      "lambda_in_smem": bool(gp.info["lambda_in_smem"])},
+            "setup": {"generate_s": t_gen, "create_s": t_create, "tile_cap": gp.info["tile_cap"],
+                      "tiles": gp.info["num_tiles"], "lambda_in_smem": bool(gp.info["lambda_in_smem"]),
+                      "lambda_hot_labels": gp.info["lambda_hot"]},
         }
         print(json.dumps(out), flush=True)
     gp.close()

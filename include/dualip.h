@@ -230,6 +230,13 @@ dl_status dl_comm_allreduce(dl_problem* p, double* buf, int64_t n);
  * is off); copies min(cap, *n) to the HOST buffer out (NULL: size query only).  Synchronous. */
 dl_status dl_debug_trace(dl_problem* p, uint64_t* out, int64_t cap, int64_t* n);
 
+/* Measurement: record the caller's CUDA events (cudaEvent_t, created by the caller) on the problem's
+ * stream immediately before (start) and after (stop) every fused-pass kernel launched outside graph
+ * capture (dl_agd_eval, dl_dual_grad*, dl_primal), so that the pass alone can be timed with
+ * cudaEventElapsedTime; the events are overwritten by each pass.  NULL, NULL stops recording.
+ * Both or neither must be given (DL_ERR_INVALID otherwise). */
+dl_status dl_set_pass_events(dl_problem* p, void* start, void* stop);
+
 /* Synchronise the problem's stream. */
 dl_status dl_sync(dl_problem* p);
 

@@ -14,8 +14,11 @@ blocks out bucket-contiguously in HBM and cuts each bucket into *tiles*
 * a bucket t >= BIG_BUCKET (length >= 256) block is a tile of its own, worked
   by a multi-warp group; smaller buckets are packed greedily, in that order,
   into tiles of at most ``tile_cap`` entries; a tile holding more than one
-  round (``round_blocks(t)`` blocks) is trimmed to whole rounds, the trimmed
+  round (``round_blocks(t, tile_cap)`` blocks) is trimmed to whole rounds, the trimmed
   blocks opening the next tile (no warp round runs with idle block groups);
+* group widths: G lanes per block (1 for t <= 3, 2 for t = 4, 2^(t-4) for t = 5..8); with tiles
+  of fewer than WIDE_CAP entries the widths of buckets 5..8 double, so that one round (32 / G
+  blocks of a bucket's typical length) still fits one tile;
 * every tile starts at an entry offset that is a multiple of 4 (16-byte TMA
   alignment); blocks inside a tile are contiguous; a block of bucket PAD_BUCKET <= t <
   BIG_BUCKET (16..255 entries) occupies its length rounded up to a multiple of 4 (padding
@@ -32,6 +35,7 @@ import math
 BIG_BUCKET = 9      # buckets >= 9 (length >= 256) are worked by multi-warp groups
 PAD_BUCKET = 5      # buckets 5..8 store blocks padded to a multiple of ALIGN entries
 ALIGN = 4           # entries (16 bytes of int32/float32)
+WIDE_CAP = 384      # tiles below this many entries use doubled group widths in buckets 5..8
 
 
 def bucket_of(s: int) -> int:
@@ -50,15 +54,20 @@ def bucket_plan(lengths):
     return dict(sorted(plan.items())), len(plan)
 
 
-def group_lanes(t: int) -> int:
-    """Lanes cooperating on one block of bucket t < BIG_BUCKET: 1 for t <= 3, 2 for t = 4, else 2^(t-4)."""
-    return 1 if t <= 3 else 2 if t == 4 else 2 ** (t - 4)
+def group_lanes(t: int, tile_cap: int) -> int:
+    """Lanes cooperating on one block of bucket t < BIG_BUCKET: 1 for t <= 3, 2 for t = 4, 2^(t-4)
+    for t = 5..8 -- doubled (2^(t-3)) when tile_cap < WIDE_CAP."""
+    if t <= 3:
+        return 1
+    if t == 4:
+        return 2
+    return 2 ** (t - 3) if tile_cap < WIDE_CAP else 2 ** (t - 4)
 
 
-def round_blocks(t: int) -> int:
+def round_blocks(t: int, tile_cap: int) -> int:
     """Blocks of bucket t < BIG_BUCKET one warp works at a time (a "round"): 32 / G with the
-    group widths G of the fused kernel (1 lane for t <= 3, 2, 2, 4, 8, 16 lanes for t = 4..8)."""
-    return 32 // group_lanes(t)
+    group widths G of the fused kernel (group_lanes)."""
+    return 32 // group_lanes(t, tile_cap)
 
 
 def stored_len(s: int) -> int:
@@ -84,7 +93,7 @@ def tile_plan(lengths, tile_cap: int):
         if t >= BIG_BUCKET:
             groups = [[i] for i in members]
         else:
-            R = round_blocks(t)
+            R = round_blocks(t, tile_cap)
             q = 0
             while q < len(members):
                 n, tot = 0, 0
@@ -141,5 +150,5 @@ def shard_bounds(row_ptr, world: int):
     return out
 
 
-__all__ = ["BIG_BUCKET", "PAD_BUCKET", "ALIGN", "bucket_of", "stored_len", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
+__all__ = ["BIG_BUCKET", "PAD_BUCKET", "ALIGN", "WIDE_CAP", "bucket_of", "stored_len", "bucket_plan", "group_lanes", "round_blocks", "tile_plan",
            "dest_labels", "shard_bounds"]

@@ -99,6 +99,7 @@ _sig = {
     "dl_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, _P]),
     "dl_comm_allreduce": (C.c_int, [_P, _P, C.c_int64]),
     "dl_debug_trace": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
+    "dl_set_pass_events": (C.c_int, [_P, _P, _P]),
     "dl_sync": (C.c_int, [_P]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -298,6 +299,12 @@ def dl_debug_trace(h):
     if n.value:
         _ck(_lib.dl_debug_trace(h, ptr(out), n.value, C.byref(n)))
     return out
+
+
+def dl_set_pass_events(h, start=None, stop=None):
+    """start/stop: torch.cuda.Event (timing enabled) or None; recorded around every fused launch."""
+    _ck(_lib.dl_set_pass_events(h, C.c_void_p(start.cuda_event if start is not None else None),
+                                C.c_void_p(stop.cuda_event if stop is not None else None)))
 
 
 def dl_sync(h):

@@ -81,6 +81,7 @@ struct dl_problem {
   double* d_gscratch = nullptr;
   int64_t gscratch_per_cta = 0;
   unsigned long long* d_trace = nullptr;  // per-CTA launch trace of the last fused pass (DUALIP_TRACE=1)
+  cudaEvent_t ev_pass[2] = {nullptr, nullptr};  // caller's events around every fused launch (dl_set_pass_events)
   // destination labels (R15): lab[j] = label of j, unlab = inverse
   bool relabeled = false;
   int32_t *d_lab = nullptr, *d_unlab = nullptr;
@@ -244,9 +245,14 @@ dl_status run_grad(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   double* acc = standalone ? p->d_acc_s : p->d_acc;
   int32_t* ctr = standalone ? p->d_ctr_s : p->d_ctr;
   if (standalone) CUDA_TRY(cudaMemsetAsync(ctr, 0, 8 * sizeof(int32_t), p->stream));
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool evs = p->ev_pass[0] && cudaStreamIsCapturing(p->stream, &cap) == cudaSuccess &&
+                   cap == cudaStreamCaptureStatusNone;
+  if (evs) CUDA_TRY(cudaEventRecord(p->ev_pass[0], p->stream));
   if (!p->plan.tiles.empty())
     CUDA_TRY(launch_fused_grad(grad_args(p, lam, gamma_ptr, gamma_val, x_out, ctr), p->ctas, p->smem,
                                p->stream));
+  if (evs) CUDA_TRY(cudaEventRecord(p->ev_pass[1], p->stream));
   // the CTA copies -> acc (every row written; the copies are left zero for the next pass)
   CUDA_TRY(launch_partial_sum(p->d_part, p->part_stride, p->part_copies, n + 4, acc, p->stream));
   return DL_OK;
@@ -1110,6 +1116,16 @@ dl_status dl_debug_trace(dl_problem* p, uint64_t* out, int64_t cap, int64_t* n) 
   DeviceGuard guard(p->device);
   CUDA_TRY(cudaMemcpyAsync(out, p->d_trace, (size_t)std::min(cap, *n) * 8, cudaMemcpyDeviceToHost, p->stream));
   CUDA_TRY(cudaStreamSynchronize(p->stream));
+  return DL_OK;
+}
+
+dl_status dl_set_pass_events(dl_problem* p, void* start, void* stop) {
+  if (!p || (!start) != (!stop)) {
+    set_error("dl_set_pass_events: NULL problem, or only one event given");
+    return DL_ERR_INVALID;
+  }
+  p->ev_pass[0] = (cudaEvent_t)start;
+  p->ev_pass[1] = (cudaEvent_t)stop;
   return DL_OK;
 }
 

@@ -39,6 +39,7 @@ namespace dl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kCandList = 128;  // per-warp candidate list: 128 x u16 entry index, then 128 x f32 dual
 constexpr int kCmax = 8;   // candidates per lane on the register fast path
 constexpr int kRcpN = 64;  // 1/n table for the Michelot threshold (sum/n within 1 ulp)
 __constant__ double c_rcp[kRcpN + 1] = {
@@ -207,23 +208,30 @@ template <int M, int LM, bool WX>
 struct Ctx {
   const GradArgs& p;
   const float* lam_s;  // duals staged in shared memory (LM != kLamGlobal)
+  const float* lam_g;  // all duals in global memory
+  int J, H;            // destinations; labels staged per family (kLamHot)
   double* acc;         // this CTA's accumulator copy
   double gamma, invgamma;
   double cx = 0.0, reg = 0.0;
   float nx = 0.f;
   __device__ Ctx(const GradArgs& pp, const float* ls, double g)
-      : p(pp), lam_s(ls), acc(pp.acc + (size_t)(blockIdx.x % pp.acc_copies) * pp.acc_stride), gamma(g),
+      : p(pp), lam_s(ls), lam_g(pp.lam), J(pp.J), H(pp.lam_hot),
+        acc(pp.acc + (size_t)(blockIdx.x % pp.acc_copies) * pp.acc_stride), gamma(g),
         invgamma(1.0 / g) {}
 
   // dual of family f at destination label j: shared memory (all, or the hot labels [0, H) of
   // the popularity order, R15) or global memory (L2-resident m*J floats)
+  // (hot: shared-memory load for labels < H, read-only global load otherwise -- two predicated loads,
+  // never a generic-address load, whose shared-window test costs ~10 instructions per lookup)
   __device__ __forceinline__ float lam(int f, int j) const {
-    if constexpr (LM == kLamSmem) return lam_s[f * p.J + j];
-    if constexpr (LM == kLamHot) {  // one generic load: shared window for hot labels, else global
-      const float* q = j < p.lam_hot ? lam_s + f * p.lam_hot + j : p.lam + (size_t)f * p.J + j;
-      return *q;
+    if constexpr (LM == kLamSmem) return lam_s[f * J + j];
+    if constexpr (LM == kLamHot) {
+      float v;
+      if (j < H) v = lam_s[f * H + j];
+      else v = __ldg(lam_g + f * J + j);
+      return v;
     }
-    return __ldg(p.lam + (size_t)f * p.J + j);
+    return __ldg(lam_g + f * J + j);
   }
   // contribution of one positive x (fp64) to A x, the objective scalars and x_out
   __device__ __forceinline__ void emit(int j, float cval, const float* av, double x, double vs, int b, int e) {
@@ -1146,16 +1154,19 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
       vs = (double)__ldg(p.vsq + b);
       ginv = C.invgamma * (double)__ldg(p.vinv + b);
     }
-    // ---- 1. fp32 pass
+    // ---- 1. fp32 pass (KEEPL: the gathered duals are kept per slot and handed to the exact
+    // rescoring with the candidates, so a dual read from L2 is read once per pass)
+    constexpr bool KEEPL = M == 1 && LM != kLamSmem && G > 1;
     float s32[E];
+    float lvs[KEEPL ? E : 1];
     float lmin = kInfF, lmag = 0.f;
     if constexpr (V4) {
-      // 4-entry groups: lane q reads groups q, q + G, q + 2G, q + 3G of the (padded) block with
+      // 4-entry groups: lane q reads groups q, q + G, .. (E/4 of them) of the (padded) block with
       // 128-bit loads; padding has c = +inf, a = 0, so its score is +inf without a test
-      static_assert(E == 16, "four 4-entry groups per lane");
+      static_assert(E % 4 == 0, "whole 4-entry groups per lane");
       const int ng = (end - start) >> 2;
 #pragma unroll
-      for (int jg = 0; jg < 4; ++jg) {
+      for (int jg = 0; jg < E / 4; ++jg) {
         const int g4 = q + jg * G;
         const int ee = start + 4 * g4;
         int4 d4 = make_int4(0, 0, 0, 0);
@@ -1179,6 +1190,7 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const float lv = C.lam(f, jj[c]);
+            if constexpr (KEEPL) lvs[4 * jg + c] = lv;
             sv[c] = fmaf(av[c], lv, sv[c]);
             if constexpr (M > 1) mg[c] = fmaf(fabsf(av[c]), fabsf(lv), mg[c]);
           }
@@ -1201,6 +1213,7 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
 #pragma unroll
         for (int f = 0; f < M; ++f) {
           const float a_ = in ? sa[f * cap + ee] : 0.f, lv = C.lam(f, j);
+          if constexpr (KEEPL) lvs[k] = lv;
           sv = fmaf(a_, lv, sv);
           if constexpr (M > 1) mg = fmaf(fabsf(a_), fabsf(lv), mg);
         }
@@ -1253,13 +1266,24 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
       }
     } else {
       uint16_t* lst = cand_s + gi * (CAP * G);
+      float* lstl = reinterpret_cast<float*>(cand_s + kCandList) + gi * (CAP * G);  // KEEPL: their duals
       if (!over) {
-        uint32_t m = cm;
         int o = excl;
-        while (m) {
-          const int k = __ffs(m) - 1;
-          m &= m - 1;
-          lst[o++] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
+        if constexpr (KEEPL) {  // static slot loop: lvs stays in registers
+#pragma unroll
+          for (int k = 0; k < E; ++k)
+            if (cm >> k & 1u) {
+              lst[o] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
+              lstl[o] = lvs[k];
+              ++o;
+            }
+        } else {
+          uint32_t m = cm;
+          while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            lst[o++] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
+          }
         }
       }
       __syncwarp();
@@ -1270,7 +1294,10 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
         ei[c] = 0;
         if (c < own) {
           ei[c] = lst[q + c * G];
-          d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
+          if constexpr (KEEPL)
+            d64[c] = (fma((double)sa[ei[c]], (double)lstl[q + c * G], (double)sc[ei[c]]) - refd) * ginv;
+          else
+            d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
         }
       }
       __syncwarp();  // the list is rewritten by the next round
@@ -1330,6 +1357,15 @@ template <int M, int LM, bool WX>
 __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
                                                        int lane, const uint16_t* rel_s, uint16_t* cand_s,
                                                        const double* rcp_s) {
+  if (wide_groups(C.p.tile_cap) && tl.bucket >= 5) {  // doubled widths (internal.h round_blocks), E = 8
+    switch (tl.bucket) {
+      case 5: small_tile_simplex<M, LM, WX, 2, 8, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      case 6: small_tile_simplex<M, LM, WX, 3, 8, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      case 7: small_tile_simplex<M, LM, WX, 4, 8, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      default: small_tile_simplex<M, LM, WX, 5, 8, true, 1>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    }
+    return;
+  }
   switch (tl.bucket) {  // (LG, E, V4, CAP): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
     case 1: small_tile_simplex<M, LM, WX, 0, 1, false, 1>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 2: small_tile_simplex<M, LM, WX, 0, 3, false, 3>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
@@ -1345,6 +1381,15 @@ __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const 
 template <int M, int LM, bool WX, bool GEN>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
                                                const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
+  if (wide_groups(C.p.tile_cap) && tl.bucket >= 5) {  // doubled widths (internal.h round_blocks), E = 8
+    switch (tl.bucket) {
+      case 5: small_tile<M, LM, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      case 6: small_tile<M, LM, WX, 3, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      case 7: small_tile<M, LM, WX, 4, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+      default: small_tile<M, LM, WX, 5, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    }
+    return;
+  }
   switch (tl.bucket) {  // (LG, E): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
     case 1:
     case 2:
@@ -1440,7 +1485,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
     char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMeta;
     const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
     const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
-    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);               // [128] candidate list
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);  // [128] candidate list (+ [128] f32 duals)
     uint64_t* bars = head->mbar[warp];
     uint64_t* dbars = head->mbar_desc[warp];
     if (lane == 0) {

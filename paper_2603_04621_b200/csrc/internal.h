@@ -24,8 +24,8 @@ constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
 constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
 // per-warp metadata in shared memory: 2 descriptor-chunk slots (2 x 128 B) + 2 block-offset slots
-// (2 x 128 B) + the round's compacted candidate list (128 x u16)
-constexpr int kMetaBytes = 768;
+// (2 x 128 B) + the round's compacted candidate list (128 x u16 entry index + 128 x f32 dual)
+constexpr int kMetaBytes = 1280;
 inline int meta_bytes(int) { return kMetaBytes; }
 
 struct alignas(16) Tile {
@@ -59,8 +59,18 @@ inline int64_t stored_len(int64_t s) {
   return (t >= kPadBucket && t < kBigBucket) ? (s + kAlign - 1) / kAlign * kAlign : s;
 }
 // blocks of a small bucket one warp works per round: 32 / G, G the group width of the fused
-// kernel (1 lane for t <= 3, then 2, 2, 4, 8, 16 lanes for t = 4..8)
-inline int round_blocks(int bucket) { return bucket <= 3 ? 32 : bucket == 4 ? 16 : 32 >> (bucket - 4); }
+// kernel (1 lane for t <= 3, 2 for t = 4, 2^(t-4) for t = 5..8 -- doubled for tiles below
+// kWideCap entries, so that a round of blocks of the bucket's typical length fits one tile)
+constexpr int kWideCap = 384;
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline bool wide_groups(int tile_cap) { return tile_cap < kWideCap; }
+inline int round_blocks(int bucket, int tile_cap) {
+  if (bucket <= 3) return 32;
+  if (bucket == 4) return 16;
+  return 32 >> (bucket - (wide_groups(tile_cap) ? 3 : 4));
+}
 inline int big_phase_of(int bucket) {  // bucket >= 12 -> phase 0 (16 warps) ... 9 -> phase 3 (2 warps)
   return bucket >= 12 ? 0 : 12 - bucket;
 }

@@ -61,7 +61,7 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
         ++n;
       }
       if (!big) {
-        const int64_t R = round_blocks(t);
+        const int64_t R = round_blocks(t, tile_cap);
         if (n > R && b + n < end) n -= n % R;
       }
       open_tile(t);

@@ -14,7 +14,7 @@ from synth.matching import CONFIGS, generate
 name = sys.argv[1] if len(sys.argv) > 1 else "1M_x_10k"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2500
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 5
-_, kind, r, u, _ = WORKLOADS[name]
+_, kind, r, u = WORKLOADS[name][:4]
 inst = generate(CONFIGS[name], threads=16)
 gp = MatchingProblem.from_instance(inst, kind=kind, r=r, u=u)
 gp.set_jacobi(gp.row_sqnorms())

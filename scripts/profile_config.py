@@ -20,7 +20,7 @@ name = sys.argv[1]
 n_src = int(sys.argv[2]) if len(sys.argv) > 2 else CONFIGS[name].num_sources
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 500
 cfg = dataclasses.replace(CONFIGS[name], num_sources=n_src)
-_, kind, r, u, _ = WORKLOADS[name]
+_, kind, r, u = WORKLOADS[name][:4]
 inst = generate(cfg, threads=16)
 gp = MatchingProblem.from_instance(inst, kind=kind, r=r, u=u)
 gp.set_jacobi(gp.row_sqnorms())

@@ -5,7 +5,7 @@ import math
 
 import numpy as np
 
-from oracle.layout import (ALIGN, BIG_BUCKET, PAD_BUCKET, bucket_of, bucket_plan, group_lanes, round_blocks,
+from oracle.layout import (ALIGN, BIG_BUCKET, PAD_BUCKET, WIDE_CAP, bucket_of, bucket_plan, group_lanes, round_blocks,
                            shard_bounds, stored_len,
                            tile_plan)
 
@@ -38,15 +38,23 @@ def test_launch_bound_and_padding_bound():
 
 
 def test_round_blocks_match_group_widths():
-    """round_blocks(t) = 32 / G(t): 32 one-lane groups for t <= 3, 16 two-lane groups for t = 4, 5,
-    then 8, 4, 2 groups of 4, 8, 16 lanes for t = 6..8; E G >= stored length of every block of the
+    """round_blocks(t, cap) = 32 / G(t, cap): 32 one-lane groups for t <= 3, 16 two-lane groups for
+    t = 4, then 2^(9-t) groups of 2^(t-4) lanes for t = 5..8 (tiles >= WIDE_CAP entries) or half
+    as many groups of twice the width (smaller tiles); E G >= stored length of every block of the
     bucket with the kernel's slots per lane E (1, 3, 7 single-lane slots for t <= 3, 8 for t = 4;
-    16 = four 4-entry groups for t >= 5)."""
-    E = {1: 1, 2: 3, 3: 7, 4: 8, 5: 16, 6: 16, 7: 16, 8: 16}
-    for t in range(1, BIG_BUCKET):
-        G = group_lanes(t)
-        assert G * round_blocks(t) == 32
-        assert E[t] * G >= stored_len(2 ** t - 1)
+    16 = four 4-entry groups for t >= 5, 8 in the wide mapping), and a round of blocks of the
+    bucket's mean length (0.75 2^t) fits one tile."""
+    for cap in (256, 380, WIDE_CAP, 460, 2048):
+        wide = cap < WIDE_CAP
+        E = {1: 1, 2: 3, 3: 7, 4: 8, 5: 16, 6: 16, 7: 16, 8: 16}
+        if wide:
+            E.update({5: 8, 6: 8, 7: 8, 8: 8})
+        for t in range(1, BIG_BUCKET):
+            G = group_lanes(t, cap)
+            assert G * round_blocks(t, cap) == 32
+            assert E[t] * G >= stored_len(2 ** t - 1)
+            if t >= PAD_BUCKET:
+                assert round_blocks(t, cap) * 0.75 * 2 ** t <= max(cap, 384)
 
 
 def test_stored_len_padding():
@@ -92,7 +100,7 @@ def test_tile_plan_invariants():
         assert covered == len(perm)
         # greedy maximality, trimmed to whole warp rounds: a tile followed by one of the same bucket
         # holds the longest run from its first block that fits tile_cap, cut down to a multiple of
-        # round_blocks(t) when the run exceeds one round
+        # round_blocks(t, cap) when the run exceeds one round
         for (a, b) in zip(tiles, tiles[1:]):
             if a[4] == b[4] and a[4] < BIG_BUCKET:
                 run, tot = 0, 0
@@ -100,7 +108,7 @@ def test_tile_plan_invariants():
                         (run == 0 or tot + stored_len(int(lens[perm[a[0] + run]])) <= cap):
                     tot += stored_len(int(lens[perm[a[0] + run]]))
                     run += 1
-                R = round_blocks(a[4])
+                R = round_blocks(a[4], cap)
                 assert a[1] == (run if run <= R else run - run % R)
         assert total >= int(lens.sum())
 
