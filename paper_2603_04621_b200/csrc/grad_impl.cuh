@@ -39,7 +39,6 @@ namespace dl {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kCandList = 128;  // per-warp candidate list: 128 x u16 entry index, then 128 x f32 dual
 constexpr int kCmax = 8;   // candidates per lane on the register fast path
 constexpr int kRcpN = 64;  // 1/n table for the Michelot threshold (sum/n within 1 ulp)
 __constant__ double c_rcp[kRcpN + 1] = {
@@ -1154,11 +1153,8 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
       vs = (double)__ldg(p.vsq + b);
       ginv = C.invgamma * (double)__ldg(p.vinv + b);
     }
-    // ---- 1. fp32 pass (KEEPL: the gathered duals are kept per slot and handed to the exact
-    // rescoring with the candidates, so a dual read from L2 is read once per pass)
-    constexpr bool KEEPL = M == 1 && LM != kLamSmem && G > 1;
+    // ---- 1. fp32 pass
     float s32[E];
-    float lvs[KEEPL ? E : 1];
     float lmin = kInfF, lmag = 0.f;
     if constexpr (V4) {
       // 4-entry groups: lane q reads groups q, q + G, .. (E/4 of them) of the (padded) block with
@@ -1190,7 +1186,6 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const float lv = C.lam(f, jj[c]);
-            if constexpr (KEEPL) lvs[4 * jg + c] = lv;
             sv[c] = fmaf(av[c], lv, sv[c]);
             if constexpr (M > 1) mg[c] = fmaf(fabsf(av[c]), fabsf(lv), mg[c]);
           }
@@ -1213,7 +1208,6 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
 #pragma unroll
         for (int f = 0; f < M; ++f) {
           const float a_ = in ? sa[f * cap + ee] : 0.f, lv = C.lam(f, j);
-          if constexpr (KEEPL) lvs[k] = lv;
           sv = fmaf(a_, lv, sv);
           if constexpr (M > 1) mg = fmaf(fabsf(a_), fabsf(lv), mg);
         }
@@ -1266,24 +1260,13 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
       }
     } else {
       uint16_t* lst = cand_s + gi * (CAP * G);
-      float* lstl = reinterpret_cast<float*>(cand_s + kCandList) + gi * (CAP * G);  // KEEPL: their duals
       if (!over) {
+        uint32_t m = cm;
         int o = excl;
-        if constexpr (KEEPL) {  // static slot loop: lvs stays in registers
-#pragma unroll
-          for (int k = 0; k < E; ++k)
-            if (cm >> k & 1u) {
-              lst[o] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
-              lstl[o] = lvs[k];
-              ++o;
-            }
-        } else {
-          uint32_t m = cm;
-          while (m) {
-            const int k = __ffs(m) - 1;
-            m &= m - 1;
-            lst[o++] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
-          }
+        while (m) {
+          const int k = __ffs(m) - 1;
+          m &= m - 1;
+          lst[o++] = (uint16_t)(start + slot_entry<LG, V4>(q, k));
         }
       }
       __syncwarp();
@@ -1294,10 +1277,7 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
         ei[c] = 0;
         if (c < own) {
           ei[c] = lst[q + c * G];
-          if constexpr (KEEPL)
-            d64[c] = (fma((double)sa[ei[c]], (double)lstl[q + c * G], (double)sc[ei[c]]) - refd) * ginv;
-          else
-            d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
+          d64[c] = (score_smem(C, sd, sc, sa, cap, ei[c]) - refd) * ginv;
         }
       }
       __syncwarp();  // the list is rewritten by the next round
@@ -1478,14 +1458,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
   // arrays and its block offsets arrive by bulk copies into a double-buffered stage.  No
   // global load sits on the critical path of a tile.
   {
-    constexpr int kChunk = 4;
+    constexpr int kChunk = 8;  // tiles per claim (one atomic) and per descriptor bulk copy
     const int s_begin = p.ph_begin[kNumBigPhases], s_end = p.ph_begin[kNumBigPhases + 1];
     char* mybuf = tilebuf + (size_t)warp * 2 * stage_bytes;
     constexpr int kMeta = kMetaBytes;
     char* meta = tilebuf + (size_t)kWarps * 2 * stage_bytes + (size_t)warp * kMeta;
     const Tile* dslot = reinterpret_cast<const Tile*>(meta);                 // [2][kChunk]
-    const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 256);   // [2][64]
-    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 512);  // [128] candidate list (+ [128] f32 duals)
+    const uint16_t* rslot = reinterpret_cast<const uint16_t*>(meta + 512);   // [2][64]
+    uint16_t* cslot = reinterpret_cast<uint16_t*>(meta + 768);  // [128] candidate list
     uint64_t* bars = head->mbar[warp];
     uint64_t* dbars = head->mbar_desc[warp];
     if (lane == 0) {
@@ -1506,7 +1486,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
       if (lane == 0 && first < s_end) {
         fence_proxy_async();
         mbar_expect_tx(&dbars[slot], kChunk * (uint32_t)sizeof(Tile));
-        tma_bulk_g2s(meta + slot * 128, p.tiles + first, kChunk * (uint32_t)sizeof(Tile), &dbars[slot]);
+        tma_bulk_g2s(meta + slot * kChunk * sizeof(Tile), p.tiles + first, kChunk * (uint32_t)sizeof(Tile),
+                     &dbars[slot]);
       }
     };
     auto issue_tile = [&](const Tile& t, int st) {
@@ -1524,7 +1505,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused_grad_kernel(const __grid_co
         for (int f = 0; f < M; ++f)
           tma_bulk_g2s_stream(dst + (size_t)p.tile_cap * (8 + 4 * f), p.a + f * p.a_stride + t.off, bytes, &bars[st],
                               pol);
-        if (rbytes) tma_bulk_g2s(meta + 256 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
+        if (rbytes) tma_bulk_g2s(meta + 512 + st * 128, p.rel_pool + t.rel_off, rbytes, &bars[st]);
       }
     };
     uint32_t phase = 0u, dphase = 0u;  // mbarrier parities, bit s for slot s (kept in registers)

@@ -23,9 +23,9 @@ constexpr int kWarps = 16;         // warps per CTA of the fused kernel
 constexpr int kThreads = kWarps * 32;
 constexpr int kNumBigPhases = 4;   // group widths 16, 8, 4, 2 warps
 constexpr int kRelMax = 63;        // tiles with fewer blocks stream their block offsets with the data
-// per-warp metadata in shared memory: 2 descriptor-chunk slots (2 x 128 B) + 2 block-offset slots
-// (2 x 128 B) + the round's compacted candidate list (128 x u16 entry index + 128 x f32 dual)
-constexpr int kMetaBytes = 1280;
+// per-warp metadata in shared memory: 2 descriptor-chunk slots (2 x 8 tiles x 32 B) + 2 block-offset
+// slots (2 x 128 B) + the round's compacted candidate list (128 x u16)
+constexpr int kMetaBytes = 1024;
 inline int meta_bytes(int) { return kMetaBytes; }
 
 struct alignas(16) Tile {

@@ -29,7 +29,7 @@ def show(tag, raw):
     tr = raw[:5 * gp.info["ctas"]].reshape(-1, 5)
     ch = raw[5 * gp.info["ctas"]:]
     t0 = tr[:, 1].min()
-    nch = (gp.info["num_tiles"] - gp.info["num_big_tiles"]) // 4
+    nch = (gp.info["num_tiles"] - gp.info["num_big_tiles"]) // 8
     tc = (ch[:nch].astype(np.int64) - int(t0)) / 1e3
     dec = [np.percentile(tc[int(nch * q / 10):int(nch * (q + 1) / 10)], 50) for q in range(10)]
     st = (tr[:, 1] - t0) / 1e3
