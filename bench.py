@@ -410,9 +410,9 @@ def main():
             pass
         peak = float(peaks.get("hbm_gbs", 6650.0))
         traffic = None
-        try:
-            prof = json.load(open(os.path.join(ROOT, "profiles", "latest_fused_ncu.json")))
-            if prof.get("workload") == args.config:
+        try:  # ncu --set full capture of this workload's fused pass (scripts/ncu_summary.py)
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(args.config)
+            if prof and world == 1:  # the capture is of the one-GPU workload
                 traffic = prof.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             pass

@@ -183,8 +183,10 @@ typedef struct {
 
 /* Resets the state: lam1 = lam2 = 0, t = 0, gamma = gamma0. */
 dl_status dl_agd_init(dl_problem* p, const dl_agd_params* prm);
-/* Runs the fused pass at the state's point mu_t into the problem's accumulator
- * (local shard only: all-reduce `acc` across ranks before dl_dual_step). */
+/* Runs the fused pass at the state's point mu_t (every CTA into its own accumulator copy, then
+ * the copies summed in CTA order, R16) and leaves the result in the problem's
+ * accumulator, overwriting it (local shard only: all-reduce `acc` across ranks before
+ * dl_dual_step). */
 dl_status dl_agd_eval(dl_problem* p);
 /* acc: device fp64 [m*J + 4] = {A x (m*J), c^T x, reg, nnz(x), 0}; count returned in n.
  * The m*J part is indexed by destination LABEL (k*J + lab[j]); all-reduce it as is. */
@@ -193,8 +195,8 @@ dl_status dl_agd_accumulator(dl_problem* p, double** acc, int64_t* n);
  * sharded, the all-reduce of the accumulator) and before dl_dual_step: grad [m*J] fp64 =
  * A x*(mu_t) - b in ORIGINAL order, obj [4] = {g(mu_t), c^T x*, reg, nnz(x*)}; device pointers. */
 dl_status dl_agd_gradient(dl_problem* p, double* grad, double* obj);
-/* One AGD step (R5-R8) from the accumulated gradient; also zeroes the
- * accumulator for the next dl_agd_eval and appends one dl_iter_record. */
+/* One AGD step (R5-R8) from the accumulated gradient; resets the pass's work
+ * counters and appends one dl_iter_record (the next dl_agd_eval overwrites the accumulator). */
 dl_status dl_dual_step(dl_problem* p);
 /* `iters` iterations of eval -> [NCCL all-reduce if dl_comm_init] -> step, captured
  * in a CUDA graph.  Asynchronous; read results with dl_agd_history / dl_agd_dual. */

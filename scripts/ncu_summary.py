@@ -2,7 +2,7 @@
 """Summarise an ncu report of the fused kernel into profiles/ (run here, no GPU needed).
 
     python scripts/ncu_summary.py gpurun_out/prof.ncu-rep profiles/r01_fused_converged.txt \
-        [--json profiles/latest_fused_ncu.json --workload 1M_x_10k --algo-bytes N]
+        [--json profiles/ncu_traffic.json --workload 1M_x_10k --algo-bytes N]
 """
 import argparse
 import collections
@@ -82,9 +82,14 @@ def main():
         for k, v in agg.most_common(25):
             lines.append(f"  {v / tot * 100:5.1f}%  L{k}: {text.get(k, '')}")
     open(a.out, "w").write("\n".join(lines) + "\n")
-    if a.json:
-        json.dump({"workload": a.workload, "kernel": kname, "dram_bytes_per_launch": traffic,
-                   "report": a.rep, "summary": a.out}, open(a.json, "w"), indent=1)
+    if a.json:  # per-workload map read by bench.py (roofline.traffic)
+        try:
+            table = json.load(open(a.json))
+        except (OSError, ValueError):
+            table = {}
+        table[a.workload] = {"kernel": kname, "dram_bytes_per_launch": traffic, "report": a.rep,
+                             "summary": a.out, "algorithmic_bytes_per_launch": a.algo_bytes}
+        json.dump(table, open(a.json, "w"), indent=1, sort_keys=True)
     print("\n".join(lines[:30]))
 
 
