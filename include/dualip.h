@@ -196,7 +196,8 @@ dl_status dl_agd_accumulator(dl_problem* p, double** acc, int64_t* n);
  * A x*(mu_t) - b in ORIGINAL order, obj [4] = {g(mu_t), c^T x*, reg, nnz(x*)}; device pointers. */
 dl_status dl_agd_gradient(dl_problem* p, double* grad, double* obj);
 /* One AGD step (R5-R8) from the accumulated gradient; resets the pass's work
- * counters and appends one dl_iter_record (the next dl_agd_eval overwrites the accumulator). */
+ * counters and appends one history record, a dl_iter_record; the next dl_agd_eval overwrites
+ * the accumulator. */
 dl_status dl_dual_step(dl_problem* p);
 /* `iters` iterations of eval -> [NCCL all-reduce if dl_comm_init] -> step, captured
  * in a CUDA graph.  Asynchronous; read results with dl_agd_history / dl_agd_dual. */
