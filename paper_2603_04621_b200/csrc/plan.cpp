@@ -5,6 +5,7 @@
 // cut into tiles: one block per tile for t >= kBigBucket (multi-warp groups), greedy
 // packing up to tile_cap entries otherwise; every tile starts 16-byte aligned.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -116,8 +117,15 @@ SmemRule smem_rule(int32_t m, int32_t J, int32_t kind) {
     r.tile_cap = (int32_t)std::min<int64_t>(cap, 2048);
     return r;
   }
-  r.tile_cap = kMinTileCap;
-  const int64_t budget = (int64_t)kSmemMax - fixed - (int64_t)kMinTileCap * per_entry;
+  // tiles of kMinTileCap entries and the rest of shared memory for hot duals; DUALIP_TILE_CAP (a
+  // multiple of 4 in [256, 2048]) trades hot duals for longer tiles (tuning experiments)
+  int64_t tc = kMinTileCap;
+  if (const char* e = std::getenv("DUALIP_TILE_CAP")) {
+    const int64_t v = std::atoll(e);
+    if (v >= kMinTileCap && v <= 2048 && v % kAlign == 0 && (int64_t)kSmemMax - fixed - v * per_entry >= 0) tc = v;
+  }
+  r.tile_cap = (int32_t)tc;
+  const int64_t budget = (int64_t)kSmemMax - fixed - tc * per_entry;
   int64_t hot = budget / (4 * (int64_t)m) / 32 * 32;
   hot = std::max<int64_t>(0, std::min<int64_t>(hot, J));
   r.hot = (int32_t)hot;

@@ -42,7 +42,7 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 B = (8 + 4 * inst.num_families) * inst.nnz
 print(f"{name} I={n_src} nnz={inst.nnz} after {iters} its: ms/eval={ms:.4f} GB/s={B / ms / 1e6:.1f} "
-      f"nnz_x={obj[3].item():.0f} tiles={gp.info['num_tiles']} tile_cap={gp.info['tile_cap']}", flush=True)
+      f"nnz_x={obj[3].item():.0f} tiles={gp.info['num_tiles']} tile_cap={gp.info['tile_cap']} hot={gp.info['lambda_hot']}", flush=True)
 torch.cuda.nvtx.range_push("fused")
 gp.dual_grad(mu, 0.01, out=(grad, obj))
 torch.cuda.nvtx.range_pop()
