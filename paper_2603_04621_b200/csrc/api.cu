@@ -229,6 +229,7 @@ GradArgs grad_args(dl_problem* p, const float* lam, const double* gamma_ptr, dou
   a.acc = p->d_part;
   a.acc_stride = p->part_stride;
   a.acc_copies = p->part_copies;
+  a.num_sms = p->num_sms;
   a.ctr = ctr;
   a.x_out = x_out;
   a.gscratch = p->d_gscratch;
@@ -429,10 +430,16 @@ dl_status create_common(const dl_problem_desc* d, dl_problem** out, bool host) {
       (s = dev_alloc(p, &p->d_tmp, MJ)) || (s = dev_alloc(p, &p->d_lab, J)) || (s = dev_alloc(p, &p->d_unlab, J)))
     return fail(s);
   if (d->v && ((s = dev_alloc(p, &p->d_vsq, nb)) || (s = dev_alloc(p, &p->d_vinv, nb)))) return fail(s);
-  // per-CTA accumulator copies: one per CTA, fewer when m J is
-  // so large that 148 copies would exceed 1 GiB (CTAs then share copies round-robin)
+  // accumulator copies: one per CTA while all of them fit in
+  // 16 MB of L2 (m J <= ~13.5k); fewer for larger m J, each shared by a run of neighbouring SMs
+  // (more would not stay in L2: the reductions would then read-modify-write DRAM)
   p->part_stride = (MJ + 4 + 31) / 32 * 32;
-  p->part_copies = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p->ctas, (int64_t)(1ll << 30) / (p->part_stride * 8)));
+  int64_t copies = std::max<int64_t>(1, std::min<int64_t>(p->ctas, (int64_t)(16ll << 20) / (p->part_stride * 8)));
+  if (const char* e = std::getenv("DUALIP_ACC_COPIES")) {  // tuning experiments
+    const int64_t v = std::atoll(e);
+    if (v >= 1 && v <= p->ctas) copies = v;
+  }
+  p->part_copies = (int32_t)copies;
   if ((s = dev_alloc(p, &p->d_part, (size_t)p->part_stride * p->part_copies))) return fail(s);
   CREATE_TRY(cudaMemsetAsync(p->d_part, 0, (size_t)p->part_stride * p->part_copies * sizeof(double), p->stream));
   // global d-scratch for blocks longer than a 16-warp group's shared scratch

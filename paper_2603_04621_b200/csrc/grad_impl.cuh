@@ -203,6 +203,15 @@ struct SmemHead {
 };
 static_assert(sizeof(SmemHead) <= 2048, "head fits the fixed smem reserve");
 
+// The accumulator copy of this CTA: copies are assigned to runs of consecutive SM ids (one per SM when
+// there are as many copies as CTAs), so that a copy shared by several CTAs is shared by neighbouring SMs.
+__device__ __forceinline__ int copy_of(const GradArgs& p) {
+  if (p.acc_copies >= (int)gridDim.x) return blockIdx.x;
+  uint32_t sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  return (int)min((uint32_t)p.acc_copies - 1u, sm * (uint32_t)p.acc_copies / max(1u, (uint32_t)p.num_sms));
+}
+
 template <int M, int LM, bool WX>
 struct Ctx {
   const GradArgs& p;
@@ -214,8 +223,8 @@ struct Ctx {
   double cx = 0.0, reg = 0.0;
   float nx = 0.f;
   __device__ Ctx(const GradArgs& pp, const float* ls, double g)
-      : p(pp), lam_s(ls), lam_g(pp.lam), J(pp.J), H(pp.lam_hot),
-        acc(pp.acc + (size_t)(blockIdx.x % pp.acc_copies) * pp.acc_stride), gamma(g),
+      : p(pp), lam_s(ls), lam_g(pp.lam), J(pp.J), H(pp.lam_hot), acc(pp.acc + (size_t)copy_of(pp) * pp.acc_stride),
+        gamma(g),
         invgamma(1.0 / g) {}
 
   // dual of family f at destination label j: shared memory (all, or the hot labels [0, H) of
@@ -1361,15 +1370,8 @@ __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const 
 template <int M, int LM, bool WX, bool GEN>
 __device__ __forceinline__ void small_dispatch(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage, int lane,
                                                const uint16_t* rel_s, uint16_t* cand_s, const double* rcp_s) {
-  if (wide_groups(C.p.tile_cap) && tl.bucket >= 5) {  // doubled widths (internal.h round_blocks), E = 8
-    switch (tl.bucket) {
-      case 5: small_tile<M, LM, WX, 2, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-      case 6: small_tile<M, LM, WX, 3, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-      case 7: small_tile<M, LM, WX, 4, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-      default: small_tile<M, LM, WX, 5, 8, GEN>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    }
-    return;
-  }
+  // box-cut / box keep the base widths also for small tiles (the wide mapping's one-slot-per-candidate
+  // solve ran 7x slower on configs[3]); a tile then holds fewer blocks than a round, which only idles lanes
   switch (tl.bucket) {  // (LG, E): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
     case 1:
     case 2:

@@ -129,6 +129,7 @@ struct GradArgs {
                            // rows [m*J + 4] by label (summed by launch_partial_sum)
   int64_t acc_stride;
   int32_t acc_copies;
+  int32_t num_sms;         // SM count (SM id -> accumulator copy when copies < CTAs)
   int32_t* ctr;            // [8] work-queue counters (zeroed before launch)
   float* x_out;            // primal output (original order) or nullptr
   double* gscratch;        // global fp64 d-scratch for blocks beyond the smem scratch

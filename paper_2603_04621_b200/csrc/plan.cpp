@@ -96,6 +96,8 @@ Plan make_plan(const int64_t* row_ptr, int64_t I, int32_t tile_cap) {
 static constexpr size_t kSmemFixed = 2048 + 1024;  // head + tail pad for over-reads past a tile
 static constexpr size_t kSmemMax = 232448;  // 227 KB opt-in per CTA on sm_100
 static constexpr int kMinTileCap = 256;      // every small block (< 256 entries) fits one tile
+static constexpr int kHotTileCap = 384;      // tiles when only the hot duals are staged (r02 sweep at J = 100k:
+                                             // 256 -> 3.57 ms, 320 -> 3.57, 384 -> 3.23, 448 -> 3.43, 512 -> 3.90)
 
 size_t fused_smem_bytes(int32_t m, int32_t kind, int32_t tile_cap, int32_t hot) {
   const size_t lam = ((size_t)m * hot * 4 + 127) / 128 * 128;
@@ -117,9 +119,10 @@ SmemRule smem_rule(int32_t m, int32_t J, int32_t kind) {
     r.tile_cap = (int32_t)std::min<int64_t>(cap, 2048);
     return r;
   }
-  // tiles of kMinTileCap entries and the rest of shared memory for hot duals; DUALIP_TILE_CAP (a
+  // tiles of kHotTileCap entries and the rest of shared memory for hot duals; DUALIP_TILE_CAP (a
   // multiple of 4 in [256, 2048]) trades hot duals for longer tiles (tuning experiments)
-  int64_t tc = kMinTileCap;
+  int64_t tc = kHotTileCap;
+  if ((int64_t)kSmemMax - fixed - tc * per_entry < (32 << 10)) tc = kMinTileCap;  // keep >= 32 KB of hot duals
   if (const char* e = std::getenv("DUALIP_TILE_CAP")) {
     const int64_t v = std::atoll(e);
     if (v >= kMinTileCap && v <= 2048 && v % kAlign == 0 && (int64_t)kSmemMax - fixed - v * per_entry >= 0) tc = v;
