@@ -216,6 +216,7 @@ template <int M, int LM, bool WX>
 struct Ctx {
   const GradArgs& p;
   const float* lam_s;  // duals staged in shared memory (LM != kLamGlobal)
+  uint32_t lam_sa;     // their shared-window address
   const float* lam_g;  // all duals in global memory
   int J, H;            // destinations; labels staged per family (kLamHot)
   double* acc;         // this CTA's accumulator copy
@@ -223,7 +224,7 @@ struct Ctx {
   double cx = 0.0, reg = 0.0;
   float nx = 0.f;
   __device__ Ctx(const GradArgs& pp, const float* ls, double g)
-      : p(pp), lam_s(ls), lam_g(pp.lam), J(pp.J), H(pp.lam_hot), acc(pp.acc + (size_t)copy_of(pp) * pp.acc_stride),
+      : p(pp), lam_s(ls), lam_sa(ls ? smem_u32(ls) : 0u), lam_g(pp.lam), J(pp.J), H(pp.lam_hot), acc(pp.acc + (size_t)copy_of(pp) * pp.acc_stride),
         gamma(g),
         invgamma(1.0 / g) {}
 
@@ -231,11 +232,20 @@ struct Ctx {
   // the popularity order, R15) or global memory (L2-resident m*J floats)
   // (hot: shared-memory load for labels < H, read-only global load otherwise -- two predicated loads,
   // never a generic-address load, whose shared-window test costs ~10 instructions per lookup)
+  // The staged duals are read with 32-bit shared-window addresses from a base kept in a register (a
+  // generic pointer into shared memory made the compiler re-derive the window base -- S2R
+  // SR_CgaCtaId, MOV, LEA -- before many lookups).  The asm is not volatile: the duals are written
+  // once before the CTA barrier and never again, so the loads may be scheduled freely.
+  __device__ __forceinline__ float lds(uint32_t a) const {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+  }
   __device__ __forceinline__ float lam(int f, int j) const {
-    if constexpr (LM == kLamSmem) return lam_s[f * J + j];
+    if constexpr (LM == kLamSmem) return lds(lam_sa + 4u * (uint32_t)(f * J + j));
     if constexpr (LM == kLamHot) {
       float v;
-      if (j < H) v = lam_s[f * H + j];
+      if (j < H) v = lds(lam_sa + 4u * (uint32_t)(f * H + j));
       else v = __ldg(lam_g + f * J + j);
       return v;
     }
@@ -1342,6 +1352,30 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
   }
 }
 
+// Blocks of one entry (bucket 1): the simplex projection of a scalar is x = clip(-s/gamma_i, 0, r)
+// (PAPER.md:125-134 with n = 1), formed directly from the exact fp64 score -- no filter, no threshold
+// search.  One block per lane, 32 per round.
+template <int M, int LM, bool WX>
+__device__ __forceinline__ void single_entry_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
+                                                          int lane) {
+  const GradArgs& p = C.p;
+  const int cap = p.tile_cap;
+  const int32_t* sd = reinterpret_cast<const int32_t*>(stage);
+  const float* sc = reinterpret_cast<const float*>(stage) + cap;
+  const float* sa = sc + cap;
+  for (int bb = lane; bb < tl.nb; bb += 32) {
+    const int b = tl.b0 + bb;
+    const int ee = bb;  // one-entry blocks are contiguous in their tile (plan.cpp): block bb is entry bb
+    double vs = 1.0, ginv = C.invgamma;  // gamma_i = gamma v_i^2
+    if (p.vsq) {
+      vs = (double)__ldg(p.vsq + b);
+      ginv = C.invgamma * (double)__ldg(p.vinv + b);
+    }
+    const double x = fmin(fmax(-score_smem(C, sd, sc, sa, cap, ee) * ginv, 0.0), p.r);
+    if (x > 0.0) emit_smem(C, sd, sc, sa, cap, ee, x, vs, b, 0);
+  }
+}
+
 template <int M, int LM, bool WX>
 __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char* stage,
                                                        int lane, const uint16_t* rel_s, uint16_t* cand_s,
@@ -1356,7 +1390,7 @@ __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const 
     return;
   }
   switch (tl.bucket) {  // (LG, E, V4, CAP): E 2^LG >= every stored length of bucket t; round_blocks(t) = 32 / 2^LG
-    case 1: small_tile_simplex<M, LM, WX, 0, 1, false, 1>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 1: single_entry_tile_simplex<M, LM, WX>(C, tl, stage, lane); break;
     case 2: small_tile_simplex<M, LM, WX, 0, 3, false, 3>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 3: small_tile_simplex<M, LM, WX, 0, 7, false, 6>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 4: small_tile_simplex<M, LM, WX, 1, 8, false, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
