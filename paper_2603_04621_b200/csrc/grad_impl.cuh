@@ -428,29 +428,32 @@ __device__ __forceinline__ int tcount(bool pred, uint32_t gmask) {
 // exactly when phi_free <= phi*); a single candidate gets x = min(phi_free, r).  emit(c, x) for x > 0.
 template <class EmitF>
 __device__ __forceinline__ void warp_michelot(const double (&d64)[8], uint32_t vm, double r, double phi_free,
-                                              EmitF&& emit) {
+                                              const double* rcp, EmitF&& emit) {
+  // |S| by one integer warp reduction per iteration (lane counts), 1/|S| from the shared table
+  // (within 1 ulp) up to kRcpN; the fp64 sum only when |S| changed
   const int nT = (int)__reduce_add_sync(kFull, (unsigned)__popc(vm));
   const int pmax = 32 - (int)__reduce_min_sync(kFull, (unsigned)__clz(vm));  // highest slot in use + 1
+  auto inv = [&](int n) { return n <= kRcpN ? rcp[n] : 1.0 / (double)n; };
   double sl = 0.0;
 #pragma unroll
   for (int c = 0; c < 8; ++c)
     if (vm >> c & 1u) sl += d64[c];
-  double phi = (r + tsum<32>(sl)) / (double)max(nT, 1);
+  double phi = (r + tsum<32>(sl)) * inv(max(nT, 1));
   int cprev = nT;
   for (int it = 0; it < 300 && nT > 1; ++it) {
-    int cnt = 0;
+    int cl = 0;
     double s2 = 0.0;
 #pragma unroll
     for (int c = 0; c < 8; ++c)
       if (c < pmax) {
         const bool in = (vm >> c & 1u) && d64[c] < phi;
-        cnt += __popc(__ballot_sync(kFull, in));
+        cl += in;
         if (in) s2 += d64[c];
       }
-    const double sm = tsum<32>(s2);
+    const int cnt = (int)__reduce_add_sync(kFull, (unsigned)cl);
     if (cnt == cprev || cnt == 0) break;
     cprev = cnt;
-    phi = (r + sm) / (double)cnt;
+    phi = (r + tsum<32>(s2)) * inv(cnt);
   }
   const double ph = nT == 1 ? phi_free : fmin(phi_free, phi);
   const double cap_x = nT == 1 ? r : kInfD;
@@ -569,7 +572,7 @@ __device__ void big_block_simplex(Ctx<M, LM, WX>& C, BigGroup& g, const Tile& tl
         vm |= 1u << c;
       }
     }
-    warp_michelot(d64, vm, p.r, -refd * ginv, [&](int c, double x) {
+    warp_michelot(d64, vm, p.r, -refd * ginv, g.head->rcp, [&](int c, double x) {
       const int64_t e = off + ee[c];
       float av[M];
 #pragma unroll
@@ -1123,7 +1126,7 @@ __device__ __forceinline__ float score32_smem(const Ctx<M, LM, WX>& C, const int
 template <int M, int LM, bool WX>
 __device__ __forceinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int32_t* sd, const float* sc,
                                                    const float* sa, int cap, int start, int end, int b, float ref,
-                                                   float thr, double vs, double ginv, int lane) {
+                                                   float thr, double vs, double ginv, int lane, const double* rcp_s) {
   double d64[8];
   uint32_t vm = 0;
   const double refd = (double)ref;
@@ -1134,7 +1137,7 @@ __device__ __forceinline__ void warp_block_simplex(Ctx<M, LM, WX>& C, const int3
     d64[c] = ok ? (score_smem(C, sd, sc, sa, cap, e) - refd) * ginv : kInfD;
     if (ok) vm |= 1u << c;
   }
-  warp_michelot(d64, vm, C.p.r, -refd * ginv, [&](int c, double x) {
+  warp_michelot(d64, vm, C.p.r, -refd * ginv, rcp_s, [&](int c, double x) {
     const int e = start + lane + 32 * c;
     emit_smem(C, sd, sc, sa, cap, e, x, vs, b, e - start);
   });
@@ -1347,7 +1350,7 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
       const int bk = __shfl_sync(kFull, b, src);
       const float rf = __shfl_sync(kFull, ref, src), th = __shfl_sync(kFull, thr, src);
       const double vsb = __shfl_sync(kFull, vs, src), gb = __shfl_sync(kFull, ginv, src);
-      warp_block_simplex<M, LM, WX>(C, sd, sc, sa, cap, s0, s1, bk, rf, th, vsb, gb, lane);
+      warp_block_simplex<M, LM, WX>(C, sd, sc, sa, cap, s0, s1, bk, rf, th, vsb, gb, lane, rcp_s);
     }
   }
 }
