@@ -1323,6 +1323,7 @@ __device__ void small_tile_simplex(Ctx<M, LM, WX>& C, const Tile& tl, const char
           s2 += d64[c];
         }
       cnt = tsum<G>(cnt);
+      if (__all_sync(kFull, done || cnt == cprev || cnt == 0)) break;  // no group needs the new sum
       s2 = tsum<G>(s2);
       if (!done) {
         if (cnt == cprev || cnt == 0) {
