@@ -28,7 +28,7 @@ def test_exports_every_declared_symbol(L):
     exported = set(re.findall(r" T (dl_\w+)", syms))
     assert declared <= exported, declared - exported
     assert declared == set(L.EXPORTED)
-    assert L.dl_abi_version() == 2
+    assert L.dl_abi_version() == 3
 
 
 def _lens_cases(rng):
