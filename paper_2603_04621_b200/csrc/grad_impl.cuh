@@ -1400,7 +1400,7 @@ __device__ __forceinline__ void small_dispatch_simplex(Ctx<M, LM, WX>& C, const 
     case 4: small_tile_simplex<M, LM, WX, 1, 8, false, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 5: small_tile_simplex<M, LM, WX, 1, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     case 6: small_tile_simplex<M, LM, WX, 2, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
-    case 7: small_tile_simplex<M, LM, WX, 3, 16, true, 4>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
+    case 7: small_tile_simplex<M, LM, WX, 3, 16, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
     default: small_tile_simplex<M, LM, WX, 4, 16, true, 2>(C, tl, stage, lane, rel_s, cand_s, rcp_s); break;
   }
 }
